@@ -119,7 +119,7 @@ def bandlimited(dims: tuple, seed: int) -> np.ndarray:
     chunk = max(1, (1 << 26) // max(1, ny * (nx // 2 + 1)))
     for z0 in range(0, nz, chunk):
         z1 = min(nz, z0 + chunk)
-        G = np.einsum("yk,zkx->zyx", Ey, Tz[z0:z1])     # (zc, ny, Kx+1)
+        G = np.matmul(Ey[None, :, :], Tz[z0:z1])          # (zc, ny, Kx+1)
         Gp = np.zeros((z1 - z0, ny, nx // 2 + 1), dtype=np.complex128)
         Gp[:, :, : Kx + 1] = G
         out[z0:z1] = nx * np.fft.irfft(Gp, n=nx, axis=2)

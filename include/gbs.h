@@ -1,0 +1,172 @@
+/*
+ * gbs.h -- C ABI of the B200-native extrapolated GBS hot path
+ *          (libgbs_b200.so, built from paper_1907_11771_b200/csrc).
+ *
+ * What it computes (§2.1, Eq. (1) "eq:GBS", lines 85-98, and the
+ * Richardson combination, lines 109-115 and 221-225; App. B R = sum c_i P_i,
+ * line 679): for every macro step ("section") of length H, starting from the
+ * current state Y, each of the m sequences k runs
+ *
+ *     y_1     = y_0 + h f(y_0),            h = H / n_k, y_0 = Y       (FE)
+ *     y_{n+1} = y_{n-1} + 2h f(y_n),       n = 1..n_k                 (LF)
+ *     y*_k    = (y_{n_k-1} + 2 y_{n_k} + y_{n_k+1}) / 4               (averaging)
+ *
+ * and the new state is  Y <- sum_k w_k y*_k,  summed in ascending n_k order.
+ * f is the method-of-lines right-hand side of a built-in linear PDE on a
+ * periodic box with centered finite differences of order 4 or 8
+ * (BASELINE.json configs; the paper itself uses a spectral derivative,
+ * see DESIGN.md):
+ *
+ *     GBS_ADV1D       u_t = -u_x                                   F = 1
+ *     GBS_ACOUSTIC2D  p_t = -(u_x + v_y), u_t = -p_x, v_t = -p_y    F = 3
+ *     GBS_WAVE3D      u_t = v, v_t = u_xx + u_yy + u_zz             F = 2
+ *
+ * All arithmetic is IEEE fp64.  Every step above runs in this library's CUDA
+ * kernels (sm_100a); there is no CPU fallback: without a usable CUDA device
+ * gbs_create fails with GBS_E_CUDA.
+ *
+ * State layout (host or device, caller-owned): SoA fp64, [F][nz][ny][nx],
+ * x fastest, unused axes of extent 1; count = F * nx * ny * nz values.
+ * Grid point i of axis d sits at i * length[d] / n[d] (periodic, S6).
+ *
+ * Ownership: the context owns every device buffer it allocates; caller
+ * arrays are read or written only during the call (never retained).  A
+ * context is not thread-safe; distinct contexts are independent.  No C++
+ * exception crosses this ABI; every int-returning call returns GBS_OK (0) or
+ * a negative GBS_E_* code, and gbs_last_error(ctx) explains the last failure.
+ */
+#ifndef GBS_B200_H
+#define GBS_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GBS_API __attribute__((visibility("default")))
+#else
+#define GBS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define GBS_OK            0
+#define GBS_E_INVAL      -1   /* bad argument: odd/duplicate/<2 n_k, m outside [1,32],
+                                 stencil order not 4/8, n[d] < 2r+1, H <= 0 or non-finite,
+                                 count mismatch, NULL pointer (named in gbs_last_error) */
+#define GBS_E_WEIGHTS    -2   /* non-finite weight, or |sum w - 1| > 1e-12 * sum |w|
+                                 (first row of Eq. (3)) */
+#define GBS_E_STATE      -3   /* gbs_advance / gbs_read_state before gbs_write_state */
+#define GBS_E_NOMEM      -4   /* device (or pinned host) allocation failed */
+#define GBS_E_CUDA       -5   /* CUDA runtime error, or no CUDA device */
+#define GBS_E_NCCL       -6   /* NCCL error (multi-GPU contexts) */
+#define GBS_E_NONFINITE  -7   /* a macro step produced a non-finite value (instability:
+                                 H beyond the imaginary stability boundary); reported by
+                                 the gbs_sync / gbs_read_state after it happened */
+#define GBS_E_UNSUPPORTED -8  /* valid request this build does not implement */
+
+/* ---- problem description ----------------------------------------------- */
+#define GBS_ADV1D       1
+#define GBS_ACOUSTIC2D  2
+#define GBS_WAVE3D      3
+
+typedef struct gbs_grid {
+    int32_t pde;        /* GBS_ADV1D | GBS_ACOUSTIC2D | GBS_WAVE3D */
+    int32_t ndim;       /* must equal the PDE's dimension (1, 2, 3) */
+    int64_t n[3];       /* grid points (nx, ny, nz); unused axes = 1 */
+    double  length[3];  /* periodic box side per axis; 0 means 1.0 (unit box) */
+} gbs_grid;
+
+/* Multi-GPU description (one process per GPU).  Pass NULL for a single GPU. */
+typedef struct gbs_dist {
+    int32_t rank;            /* this process's rank in [0, world) */
+    int32_t world;           /* number of GPUs / processes */
+    int32_t device;          /* CUDA device ordinal this rank uses */
+    int32_t groups;          /* sequence groups g (world % g == 0); 0 = planner's choice.
+                                world / g ranks share each group as z-slabs (y in 2-D) */
+    uint8_t nccl_id[128];    /* ncclUniqueId made by gbs_nccl_unique_id on rank 0 and
+                                broadcast by the caller (e.g. torch.distributed) */
+} gbs_dist;
+
+/* Plan and accounting, filled by gbs_query. */
+typedef struct gbs_info {
+    int32_t m;                   /* number of sequences */
+    int32_t fields;              /* F */
+    int32_t radius;              /* stencil radius r */
+    int32_t groups, slabs;       /* plan: g sequence groups x s slabs, g * s = world */
+    int32_t my_group, my_slab;
+    int32_t my_sequences;        /* sequences run by this rank */
+    int32_t uses_graph;          /* 1 if the macro step is replayed as a CUDA graph */
+    int64_t substeps_per_macro;  /* S = sum_k (n_k + 1): RHS-evaluating substeps */
+    int64_t my_substeps;         /* substeps this rank runs per macro step (its group's) */
+    int64_t slab_z0, slab_nz;    /* this rank's slab along the slowest axis */
+    int64_t points;              /* nx * ny * nz (global) */
+    int64_t macro_steps_done;
+    int64_t kernel_launches;     /* kernels launched by this context so far */
+    double  t;                   /* sum of H over completed gbs_advance calls */
+    double  bytes_per_point_substep;  /* algorithmic HBM bytes: 24 F */
+} gbs_info;
+
+typedef struct gbs_ctx gbs_ctx;
+
+/* Create a context: validate, plan, allocate, and (multi-GPU) join NCCL.
+ *   grid           problem description (copied)
+ *   stencil_order  4 or 8 (centered FD, radius r = order / 2)
+ *   m, n_k, w_k    step counts (even, >= 2, distinct; 1 <= m <= 32) and their
+ *                  fp64 weights (already rounded once from exact rationals by
+ *                  the caller); both copied.  Sequences with
+ *                  w_k == 0 are still executed (reading R3).
+ *   dist           NULL, or the multi-GPU description above
+ *   cuda_stream    cudaStream_t the context issues all work on (NULL = a
+ *                  stream the context creates)
+ *   out            receives the new context (NULL on failure)  */
+GBS_API int gbs_create(const gbs_grid* grid, int stencil_order, int m, const int32_t* n_k,
+               const double* w_k, const gbs_dist* dist, void* cuda_stream, gbs_ctx** out);
+
+/* Load the state Y from src (count = F*nx*ny*nz values, full grid, SoA).
+ * on_device = 1: src is device memory; 0: host memory (pinned or pageable).
+ * Multi-GPU: every rank passes the full grid and keeps its own slab. */
+GBS_API int gbs_write_state(gbs_ctx* ctx, const double* src, int64_t count, int on_device);
+
+/* Advance Y by macro_steps (>= 0) macro steps of length H (> 0, finite).
+ * Asynchronous on the context stream; t += macro_steps * H. */
+GBS_API int gbs_advance(gbs_ctx* ctx, int64_t macro_steps, double H);
+
+/* Copy the current Y (full grid) to dst; synchronizes the context stream and
+ * surfaces deferred errors (GBS_E_NONFINITE).  Multi-GPU: every rank receives
+ * the full grid (slabs are all-gathered). */
+GBS_API int gbs_read_state(gbs_ctx* ctx, double* dst, int64_t count, int on_device);
+
+/* Wait for all queued work; surfaces deferred errors. */
+GBS_API int gbs_sync(gbs_ctx* ctx);
+
+/* Release everything the context owns (NULL is a no-op). */
+GBS_API void gbs_destroy(gbs_ctx* ctx);
+
+/* Fill out128 with a fresh ncclUniqueId (call on rank 0, then broadcast). */
+GBS_API int gbs_nccl_unique_id(void* out128);
+
+/* Plan / accounting snapshot. */
+GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
+
+/* Tuning and instrumentation knobs (key -> value); unknown keys -> GBS_E_INVAL.
+ *   "graph"        1/0   replay each macro step as a CUDA graph (default 1)
+ *   "time_kernels" 1/0   record a CUDA event pair around every stencil launch
+ *                        (on the context stream) for gbs_kernel_time (default 0)
+ *   "loopback"     s     emulate s z-slabs on this GPU with device-to-device
+ *                        halo copies through the multi-GPU code path (tests)  */
+GBS_API int gbs_set_option(gbs_ctx* ctx, const char* key, int64_t value);
+
+/* Accumulated device time (ms) and launch count of the timed kernels of a class
+ * since the last reset: cls 0 = interior LF, 1 = FE (+LF1), 2 = final (average +
+ * weighted accumulate).  reset = 1 clears the counters after reading. */
+GBS_API int gbs_kernel_time(gbs_ctx* ctx, int cls, double* total_ms, int64_t* launches, int reset);
+
+GBS_API const char* gbs_strerror(int code);
+GBS_API const char* gbs_last_error(const gbs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GBS_B200_H */

@@ -1,0 +1,858 @@
+// gbs_api.cu -- the C ABI (include/gbs.h): validation, planning, device
+// memory, the per-macro-step schedule (optionally a CUDA graph), the
+// slab halo exchange and the cross-GPU combine over NCCL.
+//
+// The schedule of one macro step (Eq. (1), lines 85-98, and the
+// combination at lines 109-115, 221-225), per local slab:
+//   for each sequence k of this rank's group, ascending n_k, h = H / n_k:
+//     FE       B  = Y + h f(Y)                        (kernel MODE_FE)
+//     LF_1     C  = Y + 2h f(B)                       (MODE_LF, fresh buffer)
+//     LF_i     prev = prev + 2h f(cur), swap           (MODE_LF in place), i = 2..n_k-1
+//     final    ACC (+)= w_k/2 (prev + cur + h f(cur))  (MODE_FIN0 / MODE_FINACC)
+//   [multi-GPU] ACC <- sum over sequence groups        (ncclAllReduce, fp64 sum)
+//   swap(Y, ACC)
+// Before every stencil launch on a slabbed grid the source level's ghost
+// planes are refreshed from the neighbouring slabs (cudaMemcpyAsync between
+// local slabs in loopback mode, ncclSend/ncclRecv between ranks).
+#include "gbs.h"
+#include "gbs_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time from the process (torch's libnccl.so.2) so the
+// library loads on machines without NCCL and never links a second copy.
+// ---------------------------------------------------------------------------
+namespace nccl {
+typedef struct ncclComm* comm_t;
+typedef struct { char internal[128]; } uid_t;
+enum { ncclSuccess = 0 };
+enum { ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+typedef int (*GetUniqueId_t)(uid_t*);
+typedef int (*CommInitRank_t)(comm_t*, int, uid_t, int);
+typedef int (*CommSplit_t)(comm_t, int, int, comm_t*, void*);
+typedef int (*CommDestroy_t)(comm_t);
+typedef int (*AllReduce_t)(const void*, void*, size_t, int, int, comm_t, cudaStream_t);
+typedef int (*AllGather_t)(const void*, void*, size_t, int, comm_t, cudaStream_t);
+typedef int (*Send_t)(const void*, size_t, int, int, comm_t, cudaStream_t);
+typedef int (*Recv_t)(void*, size_t, int, int, comm_t, cudaStream_t);
+typedef int (*Group_t)(void);
+typedef const char* (*GetErrorString_t)(int);
+struct Api {
+    bool ok = false;
+    GetUniqueId_t GetUniqueId; CommInitRank_t CommInitRank; CommSplit_t CommSplit;
+    CommDestroy_t CommDestroy; AllReduce_t AllReduce; AllGather_t AllGather;
+    Send_t Send; Recv_t Recv; Group_t GroupStart, GroupEnd; GetErrorString_t GetErrorString;
+};
+static Api& api() {
+    static Api a;
+    static bool tried = false;
+    if (tried) return a;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+#define NCCL_SYM(name) a.name = (decltype(a.name))dlsym(h, "nccl" #name); if (!a.name) return a;
+    NCCL_SYM(GetUniqueId) NCCL_SYM(CommInitRank) NCCL_SYM(CommSplit) NCCL_SYM(CommDestroy)
+    NCCL_SYM(AllReduce) NCCL_SYM(AllGather) NCCL_SYM(Send) NCCL_SYM(Recv)
+    NCCL_SYM(GroupStart) NCCL_SYM(GroupEnd) NCCL_SYM(GetErrorString)
+#undef NCCL_SYM
+    a.ok = true;
+    return a;
+}
+}  // namespace nccl
+
+// ---------------------------------------------------------------------------
+struct Slab {
+    int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
+    double* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // Y, ACC, B, C (+ ghosts)
+};
+
+struct KernelTimer {
+    std::vector<cudaEvent_t> ev;      // pairs
+    std::vector<int> cls;
+    size_t used = 0;
+    double total_ms[3] = {0, 0, 0};
+    int64_t launches[3] = {0, 0, 0};
+};
+
+struct gbs_ctx {
+    // problem
+    int pde = 0, ndim = 0, F = 0, order = 0, R = 0;
+    int64_t n[3] = {1, 1, 1};
+    double len[3] = {1, 1, 1};
+    int64_t plane = 0;                // points per plane of the slowest axis
+    int64_t nslow = 0;                // extent of the slowest axis
+    int64_t points = 0;
+    // scheme (ascending n_k)
+    std::vector<int> nk_all;
+    std::vector<double> wk_all;
+    std::vector<int> my_seq;          // indices into nk_all run by this rank
+    // distribution
+    int rank = 0, world = 1, device = 0, groups = 1, slabs = 1, my_group = 0, my_slab = 0;
+    int loopback = 1;                 // local slabs on this GPU
+    nccl::comm_t comm_world = nullptr, comm_slab = nullptr, comm_group = nullptr;
+    // memory
+    std::vector<Slab> slab;
+    int64_t ghost = 0;                // ghost planes per side (R when slabbed)
+    int64_t field_stride = 0;         // doubles per field incl. ghosts
+    int yb = 0;                       // which of buf[0]/buf[1] is Y
+    int* d_flag = nullptr;
+    double* d_gather = nullptr;       // multi-GPU read_state staging
+    // execution
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool have_state = false;
+    bool use_graph = true;
+    bool time_kernels = false;
+    int zchunk_opt = 0;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    double graph_H = -1.0;
+    int64_t macro_done = 0;
+    int64_t launches = 0;
+    int64_t launches_per_macro = 0;
+    double t = 0.0;
+    KernelTimer timer;
+    std::string err;
+};
+
+static thread_local std::string g_err;
+
+static int fail(gbs_ctx* c, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    g_err = buf;
+    return code;
+}
+
+#define CU(c, call)                                                                      \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(c, GBS_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NC(c, call)                                                                         \
+    do {                                                                                    \
+        int r_ = (call);                                                                    \
+        if (r_ != nccl::ncclSuccess)                                                        \
+            return fail(c, GBS_E_NCCL, "%s failed: %s", #call, nccl::api().GetErrorString(r_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// planning
+// ---------------------------------------------------------------------------
+// Partition sequence indices into g groups with balanced sum(n_k + 1): longest
+// processing time first, then pairwise moves/swaps while the maximum drops.
+static std::vector<std::vector<int>> partition(const std::vector<int>& nk, int g) {
+    int m = (int)nk.size();
+    std::vector<int> order(m);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nk[a] > nk[b]; });
+    std::vector<std::vector<int>> grp(g);
+    std::vector<int64_t> load(g, 0);
+    for (int i : order) {
+        int best = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        grp[best].push_back(i);
+        load[best] += nk[i] + 1;
+    }
+    bool improved = true;
+    while (improved) {
+        improved = false;
+        int hi = (int)(std::max_element(load.begin(), load.end()) - load.begin());
+        for (int o = 0; o < g && !improved; ++o) {
+            if (o == hi) continue;
+            for (size_t a = 0; a < grp[hi].size() && !improved; ++a) {
+                int ia = grp[hi][a];
+                // move
+                int64_t nh = load[hi] - (nk[ia] + 1), no = load[o] + (nk[ia] + 1);
+                if (std::max(nh, no) < load[hi]) {
+                    grp[o].push_back(ia); grp[hi].erase(grp[hi].begin() + a);
+                    load[hi] = nh; load[o] = no; improved = true; break;
+                }
+                for (size_t b = 0; b < grp[o].size(); ++b) {
+                    int ib = grp[o][b];
+                    int64_t d = (int64_t)nk[ia] - nk[ib];
+                    if (d > 0 && std::max(load[hi] - d, load[o] + d) < load[hi]) {
+                        std::swap(grp[hi][a], grp[o][b]);
+                        load[hi] -= d; load[o] += d; improved = true; break;
+                    }
+                }
+            }
+        }
+    }
+    for (auto& v : grp) std::sort(v.begin(), v.end(), [&](int a, int b) { return nk[a] < nk[b]; });
+    return grp;
+}
+
+static int64_t crit_path(const std::vector<int>& nk, int g) {
+    auto grp = partition(nk, g);
+    int64_t mx = 0;
+    for (auto& v : grp) {
+        int64_t s = 0;
+        for (int i : v) s += nk[i] + 1;
+        mx = std::max(mx, s);
+    }
+    return mx;
+}
+
+// Choose g sequence groups x s slabs (g * s = world) minimising the modelled
+// per-GPU time of one macro step: stencil bytes at HBM
+// bandwidth + per-substep halo bytes at NVLink bandwidth + allreduce bytes.
+static void plan(gbs_ctx* c, int want_groups) {
+    const int W = c->world;
+    double best = 1e300;
+    int bg = 1;
+    for (int g = 1; g <= W; ++g) {
+        if (W % g) continue;
+        int s = W / g;
+        if (want_groups > 0 && g != want_groups) continue;
+        if (g > (int)c->nk_all.size()) continue;
+        if (s > 1 && (c->ndim == 1 || c->nslow % s || c->nslow / s < c->R)) continue;
+        double crit = (double)crit_path(c->nk_all, g);
+        double pts = (double)c->points / s;
+        double t_comp = crit * pts * 24.0 * c->F / 6.5e12;
+        double halo_fields = c->pde == GBS_WAVE3D ? 1.0 : 2.0;
+        double t_halo = s > 1 ? crit * (2.0 * c->R * c->plane * 8.0 * halo_fields / 7.7e11 + 2e-5) : 0.0;
+        double state = pts * c->F * 8.0;
+        double t_ar = g > 1 ? 2.0 * (g - 1) / g * state / 7.0e11 + 5e-5 : 0.0;
+        double tot = t_comp + t_halo + t_ar;
+        if (tot < best * (1 - 1e-9)) { best = tot; bg = g; }
+    }
+    c->groups = bg;
+    c->slabs = W / bg;
+}
+
+// ---------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------
+static inline double* field_ptr(gbs_ctx* c, Slab& s, int b, int f) {
+    return s.buf[b] + (int64_t)f * c->field_stride + c->ghost * c->plane;
+}
+
+static int alloc_state(gbs_ctx* c) {
+    int nloc = c->loopback;
+    int64_t total_slabs = (int64_t)c->slabs * nloc;
+    int64_t nzl = c->nslow / total_slabs;
+    c->ghost = total_slabs > 1 ? c->R : 0;
+    c->field_stride = (nzl + 2 * c->ghost) * c->plane;
+    c->slab.resize(nloc);
+    for (int v = 0; v < nloc; ++v) {
+        Slab& s = c->slab[v];
+        int64_t gidx = (int64_t)c->my_slab * nloc + v;
+        s.z0 = gidx * nzl;
+        s.nz = nzl;
+        for (int b = 0; b < 4; ++b) {
+            size_t bytes = sizeof(double) * (size_t)c->F * (size_t)c->field_stride;
+            if (cudaMalloc(&s.buf[b], bytes) != cudaSuccess)
+                return fail(c, GBS_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
+            CU(c, cudaMemsetAsync(s.buf[b], 0, bytes, c->stream));
+        }
+    }
+    CU(c, cudaMalloc(&c->d_flag, sizeof(int)));
+    CU(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    return GBS_OK;
+}
+
+static void free_state(gbs_ctx* c) {
+    for (auto& s : c->slab)
+        for (int b = 0; b < 4; ++b)
+            if (s.buf[b]) { cudaFree(s.buf[b]); s.buf[b] = nullptr; }
+    c->slab.clear();
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+// ---------------------------------------------------------------------------
+struct StepOperands {
+    int S, P, O;          // buffer indices (0..3) of the current level, previous level, output
+    int mode;
+    double cf, wh;
+    bool flag;
+};
+
+template <int R, int MODE, bool SLAB>
+static void launch_wave3d(const gbs::Wave3DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
+    if (vx2) gbs::wave3d_step<R, MODE, 2, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
+    else gbs::wave3d_step<R, MODE, 1, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
+}
+template <int R, int MODE, bool SLAB>
+static void launch_ac2d(const gbs::Acoustic2DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
+    if (vx2) gbs::acoustic2d_step<R, MODE, 2, 128, SLAB><<<grid, 128, 0, st>>>(a);
+    else gbs::acoustic2d_step<R, MODE, 1, 128, SLAB><<<grid, 128, 0, st>>>(a);
+}
+
+static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
+    if (zchunk_opt > 0) return (int)std::min<int64_t>(zchunk_opt, extent);
+    // aim at >= ~16 resident waves of CTAs so the tail stays small, with
+    // chunks of at least 32 planes so the 2r warm-up planes stay cheap
+    const int64_t target = 148 * 2 * 16;
+    int64_t chunks = std::max<int64_t>(1, (target + tiles - 1) / tiles);
+    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, extent / 32));
+    return (int)((extent + chunks - 1) / chunks);
+}
+
+static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
+    const bool slab = c->ghost > 0;
+    int* flag = op.flag ? c->d_flag : nullptr;
+    if (c->pde == GBS_WAVE3D) {
+        gbs::Wave3DArgs a;
+        a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1);
+        a.Pu = field_ptr(c, s, op.P, 0); a.Pv = field_ptr(c, s, op.P, 1);
+        a.Ou = field_ptr(c, s, op.O, 0); a.Ov = field_ptr(c, s, op.O, 1);
+        a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
+        a.plane = c->plane;
+        const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
+        a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
+        a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        const bool vx2 = (c->n[0] % 2) == 0;
+        const int TX = vx2 ? 64 : 32, TY = 16;
+        int64_t tx = (c->n[0] + TX - 1) / TX, ty = (c->n[1] + TY - 1) / TY;
+        a.zchunk = chunk_for(tx * ty, s.nz, c->zchunk_opt);
+        dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
+#define W3(RR, SL)                                                                   \
+        switch (op.mode) {                                                           \
+            case gbs::MODE_FE: launch_wave3d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_LF: launch_wave3d<RR, gbs::MODE_LF, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_FIN0: launch_wave3d<RR, gbs::MODE_FIN0, SL>(a, grid, vx2, c->stream); break; \
+            default: launch_wave3d<RR, gbs::MODE_FINACC, SL>(a, grid, vx2, c->stream); break;         \
+        }
+        if (c->R == 2) { if (slab) { W3(2, true) } else { W3(2, false) } }
+        else { if (slab) { W3(4, true) } else { W3(4, false) } }
+#undef W3
+    } else if (c->pde == GBS_ACOUSTIC2D) {
+        gbs::Acoustic2DArgs a;
+        for (int f = 0; f < 3; ++f) {
+            a.S[f] = field_ptr(c, s, op.S, f);
+            a.P[f] = field_ptr(c, s, op.P, f);
+            a.O[f] = field_ptr(c, s, op.O, f);
+        }
+        a.nx = (int)c->n[0]; a.ny = (int)s.nz;
+        a.sx = c->n[0] / c->len[0]; a.sy = c->n[1] / c->len[1];
+        a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        const bool vx2 = (c->n[0] % 2) == 0;
+        const int TX = vx2 ? 256 : 128;
+        int64_t tx = (c->n[0] + TX - 1) / TX;
+        a.ychunk = chunk_for(tx, s.nz, c->zchunk_opt);
+        dim3 grid((unsigned)tx, (unsigned)((s.nz + a.ychunk - 1) / a.ychunk));
+#define A2(RR, SL)                                                                   \
+        switch (op.mode) {                                                           \
+            case gbs::MODE_FE: launch_ac2d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_LF: launch_ac2d<RR, gbs::MODE_LF, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_FIN0: launch_ac2d<RR, gbs::MODE_FIN0, SL>(a, grid, vx2, c->stream); break; \
+            default: launch_ac2d<RR, gbs::MODE_FINACC, SL>(a, grid, vx2, c->stream); break;         \
+        }
+        if (c->R == 2) { if (slab) { A2(2, true) } else { A2(2, false) } }
+        else { if (slab) { A2(4, true) } else { A2(4, false) } }
+#undef A2
+    } else {
+        gbs::Adv1DArgs a;
+        a.S = field_ptr(c, s, op.S, 0); a.P = field_ptr(c, s, op.P, 0); a.O = field_ptr(c, s, op.O, 0);
+        a.nx = (int)c->n[0]; a.sx = c->n[0] / c->len[0];
+        a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        constexpr int NT = 256;
+        dim3 grid((unsigned)((c->n[0] + NT - 1) / NT));
+#define A1(RR)                                                                            \
+        switch (op.mode) {                                                                \
+            case gbs::MODE_FE: gbs::adv1d_step<RR, gbs::MODE_FE, NT><<<grid, NT, 0, c->stream>>>(a); break;   \
+            case gbs::MODE_LF: gbs::adv1d_step<RR, gbs::MODE_LF, NT><<<grid, NT, 0, c->stream>>>(a); break;   \
+            case gbs::MODE_FIN0: gbs::adv1d_step<RR, gbs::MODE_FIN0, NT><<<grid, NT, 0, c->stream>>>(a); break; \
+            default: gbs::adv1d_step<RR, gbs::MODE_FINACC, NT><<<grid, NT, 0, c->stream>>>(a); break;         \
+        }
+        if (c->R == 2) { A1(2) } else { A1(4) }
+#undef A1
+    }
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// halo exchange of buffer b's halo fields (ghost planes along the slowest axis)
+// ---------------------------------------------------------------------------
+static int exchange_halo(gbs_ctx* c, int b) {
+    if (c->ghost == 0) return GBS_OK;
+    const int64_t G = c->ghost, P = c->plane;
+    const size_t cnt = (size_t)(G * P);
+    std::vector<int> fields;
+    if (c->pde == GBS_WAVE3D) fields = {0};
+    else fields = {0, 2};                       // acoustics: p and v cross the y slabs
+    const int nloc = c->loopback;
+    const int S = c->slabs * nloc;              // global slab count
+    if (c->slabs == 1) {
+        // all slabs local: device-to-device copies
+        for (int v = 0; v < nloc; ++v) {
+            Slab& me = c->slab[v];
+            Slab& lo = c->slab[(v - 1 + nloc) % nloc];
+            Slab& hi = c->slab[(v + 1) % nloc];
+            for (int f : fields) {
+                double* mine = field_ptr(c, me, b, f);
+                // bottom ghosts <- lower neighbour's top interior planes
+                CU(c, cudaMemcpyAsync(mine - G * P, field_ptr(c, lo, b, f) + (lo.nz - G) * P,
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                // top ghosts <- upper neighbour's bottom interior planes
+                CU(c, cudaMemcpyAsync(mine + me.nz * P, field_ptr(c, hi, b, f),
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+            }
+        }
+        return GBS_OK;
+    }
+    if (nloc != 1) return fail(c, GBS_E_UNSUPPORTED, "loopback slabs with multi-GPU slabs");
+    (void)S;
+    auto& A = nccl::api();
+    const int lo = (c->my_slab - 1 + c->slabs) % c->slabs, hi = (c->my_slab + 1) % c->slabs;
+    Slab& me = c->slab[0];
+    NC(c, A.GroupStart());
+    for (int f : fields) {
+        double* mine = field_ptr(c, me, b, f);
+        NC(c, A.Send(mine, cnt, nccl::ncclFloat64, lo, c->comm_slab, c->stream));                  // my bottom -> lo's top ghosts
+        NC(c, A.Send(mine + (me.nz - G) * P, cnt, nccl::ncclFloat64, hi, c->comm_slab, c->stream)); // my top -> hi's bottom ghosts
+        NC(c, A.Recv(mine - G * P, cnt, nccl::ncclFloat64, lo, c->comm_slab, c->stream));
+        NC(c, A.Recv(mine + me.nz * P, cnt, nccl::ncclFloat64, hi, c->comm_slab, c->stream));
+    }
+    NC(c, A.GroupEnd());
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// timing instrumentation (event pairs on the context stream)
+// ---------------------------------------------------------------------------
+static int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev) {
+    KernelTimer& T = c->timer;
+    if (T.used + 2 > T.ev.size()) {
+        for (int i = 0; i < 256; ++i) {
+            cudaEvent_t e;
+            CU(c, cudaEventCreate(&e));
+            T.ev.push_back(e);
+        }
+        T.cls.resize(T.ev.size() / 2);
+    }
+    CU(c, cudaEventRecord(T.ev[T.used], c->stream));
+    T.cls[T.used / 2] = cls;
+    *end_ev = T.ev[T.used + 1];
+    T.used += 2;
+    return GBS_OK;
+}
+
+static int step(gbs_ctx* c, int cls, const StepOperands& op) {
+    int rc;
+    if ((rc = exchange_halo(c, op.S))) return rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
+    for (auto& s : c->slab)
+        if ((rc = launch_step(c, s, op))) return rc;
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    return GBS_OK;
+}
+
+static int harvest_timer(gbs_ctx* c) {
+    KernelTimer& T = c->timer;
+    if (!T.used) return GBS_OK;
+    CU(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < T.used; i += 2) {
+        float ms = 0.f;
+        CU(c, cudaEventElapsedTime(&ms, T.ev[i], T.ev[i + 1]));
+        int k = T.cls[i / 2];
+        T.total_ms[k] += ms;
+        T.launches[k] += 1;
+    }
+    T.used = 0;
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one macro step (enqueue only)
+// ---------------------------------------------------------------------------
+static int enqueue_macro(gbs_ctx* c, double H) {
+    const int Y = c->yb, ACC = 1 - c->yb, B = 2, C = 3;
+    const int64_t l0 = c->launches;
+    int rc;
+    bool first = true;
+    for (size_t q = 0; q < c->my_seq.size(); ++q) {
+        const int k = c->my_seq[q];
+        const int n = c->nk_all[k];
+        const double h = H / (double)n;
+        const bool last = (q + 1 == c->my_seq.size());
+        if ((rc = step(c, 1, {Y, Y, B, gbs::MODE_FE, h, 0.0, false}))) return rc;            // y1
+        if ((rc = step(c, 0, {B, Y, C, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;      // y2
+        int prev = B, cur = C;
+        for (int i = 2; i <= n - 1; ++i) {                                                    // y3..yN
+            if ((rc = step(c, 0, {cur, prev, prev, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;
+            std::swap(prev, cur);
+        }
+        StepOperands fin{cur, prev, ACC, first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, h,
+                         0.5 * c->wk_all[k], last};
+        if ((rc = step(c, 2, fin))) return rc;
+        first = false;
+    }
+    if (c->groups > 1) {
+        auto& A = nccl::api();
+        Slab& s = c->slab[0];
+        NC(c, A.GroupStart());
+        for (int f = 0; f < c->F; ++f) {
+            double* p = field_ptr(c, s, ACC, f);
+            NC(c, A.AllReduce(p, p, (size_t)(s.nz * c->plane), nccl::ncclFloat64, nccl::ncclSum,
+                              c->comm_group, c->stream));
+        }
+        NC(c, A.GroupEnd());
+    }
+    c->yb = ACC;
+    c->launches_per_macro = c->launches - l0;
+    return GBS_OK;
+}
+
+static int check_flag(gbs_ctx* c) {
+    int h = 0;
+    CU(c, cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(c, cudaStreamSynchronize(c->stream));
+    if (h) {
+        CU(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        return fail(c, GBS_E_NONFINITE, "non-finite state after a macro step (H beyond the stability limit?)");
+    }
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* gbs_strerror(int code) {
+    switch (code) {
+        case GBS_OK: return "ok";
+        case GBS_E_INVAL: return "invalid argument";
+        case GBS_E_WEIGHTS: return "invalid extrapolation weights";
+        case GBS_E_STATE: return "state not written";
+        case GBS_E_NOMEM: return "out of memory";
+        case GBS_E_CUDA: return "CUDA error";
+        case GBS_E_NCCL: return "NCCL error";
+        case GBS_E_NONFINITE: return "non-finite state";
+        case GBS_E_UNSUPPORTED: return "unsupported";
+        default: return "unknown error";
+    }
+}
+
+const char* gbs_last_error(const gbs_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+int gbs_nccl_unique_id(void* out128) {
+    if (!out128) return fail(nullptr, GBS_E_INVAL, "out128 is NULL");
+    auto& A = nccl::api();
+    if (!A.ok) return fail(nullptr, GBS_E_NCCL, "libnccl.so.2 not found");
+    nccl::uid_t id;
+    int r = A.GetUniqueId(&id);
+    if (r) return fail(nullptr, GBS_E_NCCL, "ncclGetUniqueId: %s", A.GetErrorString(r));
+    memcpy(out128, &id, 128);
+    return GBS_OK;
+}
+
+void gbs_destroy(gbs_ctx* c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
+    free_state(c);
+    if (c->d_flag) cudaFree(c->d_flag);
+    if (c->d_gather) cudaFree(c->d_gather);
+    for (auto e : c->timer.ev) cudaEventDestroy(e);
+    auto& A = nccl::api();
+    if (A.ok) {
+        if (c->comm_group) A.CommDestroy(c->comm_group);
+        if (c->comm_slab) A.CommDestroy(c->comm_slab);
+        if (c->comm_world) A.CommDestroy(c->comm_world);
+    }
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+static int build_ctx(gbs_ctx* c) {
+    int rc;
+    // the sequences of this rank's group
+    auto grp = partition(c->nk_all, c->groups);
+    c->my_seq = grp[c->my_group];
+    if ((rc = alloc_state(c))) return rc;
+    return GBS_OK;
+}
+
+int gbs_create(const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, const double* w_k,
+               const gbs_dist* dist, void* cuda_stream, gbs_ctx** out) {
+    if (!out) return fail(nullptr, GBS_E_INVAL, "out is NULL");
+    *out = nullptr;
+    if (!g || !n_k || !w_k) return fail(nullptr, GBS_E_INVAL, "grid, n_k or w_k is NULL");
+    gbs_ctx* c = new (std::nothrow) gbs_ctx();
+    if (!c) return fail(nullptr, GBS_E_NOMEM, "host allocation failed");
+    auto bail = [&](int code) { g_err = c->err; gbs_destroy(c); return code; };
+
+    // ---- validate the problem
+    c->pde = g->pde;
+    if (g->pde == GBS_ADV1D) { c->ndim = 1; c->F = 1; }
+    else if (g->pde == GBS_ACOUSTIC2D) { c->ndim = 2; c->F = 3; }
+    else if (g->pde == GBS_WAVE3D) { c->ndim = 3; c->F = 2; }
+    else return bail(fail(c, GBS_E_INVAL, "grid.pde=%d is not a known PDE", g->pde));
+    if (g->ndim != c->ndim) return bail(fail(c, GBS_E_INVAL, "grid.ndim=%d does not match the PDE", g->ndim));
+    if (stencil_order != 4 && stencil_order != 8)
+        return bail(fail(c, GBS_E_INVAL, "stencil_order=%d (must be 4 or 8)", stencil_order));
+    c->order = stencil_order;
+    c->R = stencil_order / 2;
+    for (int d = 0; d < 3; ++d) {
+        c->n[d] = g->n[d];
+        c->len[d] = g->length[d] == 0.0 ? 1.0 : g->length[d];
+        if (d < c->ndim) {
+            if (g->n[d] < 2 * c->R + 1)
+                return bail(fail(c, GBS_E_INVAL, "grid.n[%d]=%lld < 2r+1=%d", d, (long long)g->n[d], 2 * c->R + 1));
+            if (g->n[d] > (int64_t)1 << 30)
+                return bail(fail(c, GBS_E_INVAL, "grid.n[%d]=%lld too large", d, (long long)g->n[d]));
+            if (!(c->len[d] > 0.0) || !std::isfinite(c->len[d]))
+                return bail(fail(c, GBS_E_INVAL, "grid.length[%d] must be positive", d));
+        } else if (g->n[d] != 1) {
+            return bail(fail(c, GBS_E_INVAL, "grid.n[%d] must be 1 for a %d-D PDE", d, c->ndim));
+        }
+    }
+    c->points = c->n[0] * c->n[1] * c->n[2];
+    c->nslow = c->n[c->ndim - 1];
+    c->plane = c->points / c->nslow;
+
+    // ---- validate the scheme
+    if (m < 1 || m > 32) return bail(fail(c, GBS_E_INVAL, "m=%d (must be 1..32)", m));
+    std::vector<std::pair<int, double>> seq;
+    for (int i = 0; i < m; ++i) {
+        if (n_k[i] < 2 || n_k[i] % 2)
+            return bail(fail(c, GBS_E_INVAL, "n_k[%d]=%d must be even and >= 2", i, n_k[i]));
+        if (n_k[i] > 1 << 20) return bail(fail(c, GBS_E_INVAL, "n_k[%d]=%d too large", i, n_k[i]));
+        for (int j = 0; j < i; ++j)
+            if (n_k[j] == n_k[i]) return bail(fail(c, GBS_E_INVAL, "n_k[%d]=n_k[%d]=%d duplicate", j, i, n_k[i]));
+        if (!std::isfinite(w_k[i])) return bail(fail(c, GBS_E_WEIGHTS, "w_k[%d] is not finite", i));
+        seq.push_back({n_k[i], w_k[i]});
+    }
+    std::sort(seq.begin(), seq.end());
+    double sw = 0.0, sa = 0.0;
+    for (auto& p : seq) { sw += p.second; sa += std::fabs(p.second); }
+    if (!(std::fabs(sw - 1.0) <= 1e-12 * sa))
+        return bail(fail(c, GBS_E_WEIGHTS, "sum of weights = %.17g (must be 1 within 1e-12 * sum|w|)", sw));
+    for (auto& p : seq) { c->nk_all.push_back(p.first); c->wk_all.push_back(p.second); }
+
+    // ---- device / stream
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+        return bail(fail(c, GBS_E_CUDA, "no CUDA device available (this library has no CPU path)"));
+    if (dist) {
+        if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+            return bail(fail(c, GBS_E_INVAL, "dist rank=%d world=%d", dist->rank, dist->world));
+        c->rank = dist->rank; c->world = dist->world; c->device = dist->device;
+        if (dist->groups < 0 || (dist->groups > 0 && dist->world % dist->groups))
+            return bail(fail(c, GBS_E_INVAL, "dist.groups=%d must divide world=%d", dist->groups, dist->world));
+    } else {
+        cudaGetDevice(&c->device);
+    }
+    if (c->device < 0 || c->device >= ndev)
+        return bail(fail(c, GBS_E_INVAL, "device %d out of range (%d devices)", c->device, ndev));
+    if (cudaSetDevice(c->device) != cudaSuccess)
+        return bail(fail(c, GBS_E_CUDA, "cudaSetDevice(%d) failed", c->device));
+    if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
+    else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(c, GBS_E_CUDA, "cudaStreamCreate failed"));
+        c->own_stream = true;
+    }
+
+    // ---- plan + communicators
+    plan(c, dist ? dist->groups : 0);
+    if (c->groups * c->slabs != c->world)
+        return bail(fail(c, GBS_E_INVAL, "no valid plan: groups=%d does not fit world=%d (m=%d, slowest axis %lld)",
+                         dist ? dist->groups : 0, c->world, m, (long long)c->nslow));
+    c->my_group = c->rank / c->slabs;
+    c->my_slab = c->rank % c->slabs;
+    if (c->world > 1) {
+        auto& A = nccl::api();
+        if (!A.ok) return bail(fail(c, GBS_E_NCCL, "libnccl.so.2 not found"));
+        nccl::uid_t id;
+        memcpy(&id, dist->nccl_id, 128);
+        int r = A.CommInitRank(&c->comm_world, c->world, id, c->rank);
+        if (r) return bail(fail(c, GBS_E_NCCL, "ncclCommInitRank: %s", A.GetErrorString(r)));
+        if (c->slabs > 1) {
+            r = A.CommSplit(c->comm_world, c->my_group, c->my_slab, &c->comm_slab, nullptr);
+            if (r) return bail(fail(c, GBS_E_NCCL, "ncclCommSplit(slab): %s", A.GetErrorString(r)));
+        }
+        if (c->groups > 1) {
+            r = A.CommSplit(c->comm_world, c->my_slab, c->my_group, &c->comm_group, nullptr);
+            if (r) return bail(fail(c, GBS_E_NCCL, "ncclCommSplit(group): %s", A.GetErrorString(r)));
+        }
+        c->use_graph = false;   // NCCL calls stay outside graphs
+    }
+    int rc = build_ctx(c);
+    if (rc) return bail(rc);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(c, GBS_E_CUDA, "init sync failed"));
+    *out = c;
+    return GBS_OK;
+}
+
+int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
+    if (!c || !key) return fail(c, GBS_E_INVAL, "ctx or key is NULL");
+    std::string k(key);
+    auto drop_graphs = [&]() {
+        for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+        c->graph_H = -1.0;
+    };
+    if (k == "graph") { c->use_graph = value != 0 && c->world == 1; drop_graphs(); return GBS_OK; }
+    if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "loopback") {
+        if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");
+        if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback needs a single-GPU context");
+        if (c->ndim == 1 && value > 1) return fail(c, GBS_E_UNSUPPORTED, "1-D grids are not slabbed");
+        if (c->nslow % value || c->nslow / value < c->R)
+            return fail(c, GBS_E_INVAL, "loopback=%lld must divide the slowest axis (%lld) into slabs >= r",
+                        (long long)value, (long long)c->nslow);
+        cudaStreamSynchronize(c->stream);
+        drop_graphs();
+        free_state(c);
+        if (c->d_flag) { cudaFree(c->d_flag); c->d_flag = nullptr; }
+        c->loopback = (int)value;
+        c->have_state = false;
+        return alloc_state(c);
+    }
+    return fail(c, GBS_E_INVAL, "unknown option '%s'", key);
+}
+
+int gbs_write_state(gbs_ctx* c, const double* src, int64_t count, int on_device) {
+    if (!c || !src) return fail(c, GBS_E_INVAL, "ctx or src is NULL");
+    if (count != c->F * c->points)
+        return fail(c, GBS_E_INVAL, "count=%lld, expected F*points=%lld", (long long)count, (long long)(c->F * c->points));
+    CU(c, cudaSetDevice(c->device));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (auto& s : c->slab)
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(field_ptr(c, s, c->yb, f), src + (int64_t)f * c->points + s.z0 * c->plane,
+                                  sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
+    c->have_state = true;
+    return GBS_OK;
+}
+
+int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
+    if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_advance before gbs_write_state");
+    if (macro_steps < 0) return fail(c, GBS_E_INVAL, "macro_steps=%lld < 0", (long long)macro_steps);
+    if (!(H > 0.0) || !std::isfinite(H)) return fail(c, GBS_E_INVAL, "H=%g must be positive and finite", H);
+    CU(c, cudaSetDevice(c->device));
+    int rc;
+    const bool graph = c->use_graph && !c->time_kernels && macro_steps > 0;
+    if (graph && c->graph_H != H) {
+        for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+        c->graph_H = H;
+    }
+    for (int64_t i = 0; i < macro_steps; ++i) {
+        if (graph) {
+            const int par = c->yb;
+            if (!c->gexec[par]) {
+                cudaGraph_t gr;
+                CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+                rc = enqueue_macro(c, H);
+                cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+                if (rc) { if (e == cudaSuccess) cudaGraphDestroy(gr); return rc; }
+                if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+                e = cudaGraphInstantiate(&c->gexec[par], gr, 0);
+                cudaGraphDestroy(gr);
+                if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+                c->yb = par;          // capture does not execute: rewind the parity
+                c->launches -= c->launches_per_macro;
+            }
+            CU(c, cudaGraphLaunch(c->gexec[par], c->stream));
+            c->launches += c->launches_per_macro;
+            c->yb = 1 - par;
+        } else {
+            if ((rc = enqueue_macro(c, H))) return rc;
+        }
+        c->macro_done++;
+        c->t += H;
+    }
+    return GBS_OK;
+}
+
+int gbs_sync(gbs_ctx* c) {
+    if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    CU(c, cudaSetDevice(c->device));
+    CU(c, cudaStreamSynchronize(c->stream));
+    return check_flag(c);
+}
+
+int gbs_read_state(gbs_ctx* c, double* dst, int64_t count, int on_device) {
+    if (!c || !dst) return fail(c, GBS_E_INVAL, "ctx or dst is NULL");
+    if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_read_state before gbs_write_state");
+    if (count != c->F * c->points)
+        return fail(c, GBS_E_INVAL, "count=%lld, expected F*points=%lld", (long long)count, (long long)(c->F * c->points));
+    CU(c, cudaSetDevice(c->device));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (c->slabs == 1) {
+        for (auto& s : c->slab)
+            for (int f = 0; f < c->F; ++f)
+                CU(c, cudaMemcpyAsync(dst + (int64_t)f * c->points + s.z0 * c->plane, field_ptr(c, s, c->yb, f),
+                                      sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
+    } else {
+        auto& A = nccl::api();
+        Slab& s = c->slab[0];
+        const size_t slab_cnt = (size_t)(s.nz * c->plane);
+        if (!c->d_gather) CU(c, cudaMalloc(&c->d_gather, sizeof(double) * (size_t)c->points));
+        for (int f = 0; f < c->F; ++f) {
+            NC(c, A.AllGather(field_ptr(c, s, c->yb, f), c->d_gather, slab_cnt, nccl::ncclFloat64,
+                              c->comm_slab, c->stream));
+            CU(c, cudaMemcpyAsync(dst + (int64_t)f * c->points, c->d_gather, sizeof(double) * (size_t)c->points,
+                                  kind, c->stream));
+        }
+    }
+    int rc = gbs_sync(c);
+    if (rc) return rc;
+    return harvest_timer(c);
+}
+
+int gbs_query(const gbs_ctx* c, gbs_info* info) {
+    if (!c || !info) return fail(const_cast<gbs_ctx*>(c), GBS_E_INVAL, "ctx or info is NULL");
+    memset(info, 0, sizeof(*info));
+    info->m = (int)c->nk_all.size();
+    info->fields = c->F;
+    info->radius = c->R;
+    info->groups = c->groups;
+    info->slabs = c->slabs * c->loopback;
+    info->my_group = c->my_group;
+    info->my_slab = c->my_slab;
+    info->my_sequences = (int)c->my_seq.size();
+    info->uses_graph = c->use_graph && !c->time_kernels;
+    int64_t S = 0, mine = 0;
+    for (int n : c->nk_all) S += n + 1;
+    for (int k : c->my_seq) mine += c->nk_all[k] + 1;
+    info->substeps_per_macro = S;
+    info->my_substeps = mine;
+    info->slab_z0 = c->slab.empty() ? 0 : c->slab[0].z0;
+    info->slab_nz = c->slab.empty() ? 0 : c->slab[0].nz * c->loopback;
+    info->points = c->points;
+    info->macro_steps_done = c->macro_done;
+    info->kernel_launches = c->launches;
+    info->t = c->t;
+    info->bytes_per_point_substep = 24.0 * c->F;
+    return GBS_OK;
+}
+
+int gbs_kernel_time(gbs_ctx* c, int cls, double* total_ms, int64_t* launches, int reset) {
+    if (!c || cls < 0 || cls > 2) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
+    int rc = harvest_timer(c);
+    if (rc) return rc;
+    if (total_ms) *total_ms = c->timer.total_ms[cls];
+    if (launches) *launches = c->timer.launches[cls];
+    if (reset) { c->timer.total_ms[cls] = 0; c->timer.launches[cls] = 0; }
+    return GBS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+"""Thin Python binding of libgbs_b200.so (include/gbs.h): argument marshalling only.
+
+Every function has the C name and forwards to the C ABI; every step of the hot
+path runs in the library's CUDA kernels.  There is no fallback: if the shared
+library is missing or a CUDA device is absent the calls raise.
+
+Device buffers are torch CUDA tensors (plumbing), host buffers numpy arrays
+or CPU tensors; the stream is torch's current CUDA stream unless given.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _build
+
+GBS_OK = 0
+GBS_E_INVAL, GBS_E_WEIGHTS, GBS_E_STATE, GBS_E_NOMEM = -1, -2, -3, -4
+GBS_E_CUDA, GBS_E_NCCL, GBS_E_NONFINITE, GBS_E_UNSUPPORTED = -5, -6, -7, -8
+PDE = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
+FIELDS = {"adv1d": 1, "acoustic2d": 3, "wave3d": 2}
+NDIM = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
+
+EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_sync",
+           "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_set_option",
+           "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
+
+
+class gbs_grid(ctypes.Structure):
+    _fields_ = [("pde", ctypes.c_int32), ("ndim", ctypes.c_int32),
+                ("n", ctypes.c_int64 * 3), ("length", ctypes.c_double * 3)]
+
+
+class gbs_dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("groups", ctypes.c_int32), ("nccl_id", ctypes.c_uint8 * 128)]
+
+
+class gbs_info(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("fields", ctypes.c_int32), ("radius", ctypes.c_int32),
+                ("groups", ctypes.c_int32), ("slabs", ctypes.c_int32),
+                ("my_group", ctypes.c_int32), ("my_slab", ctypes.c_int32),
+                ("my_sequences", ctypes.c_int32), ("uses_graph", ctypes.c_int32),
+                ("substeps_per_macro", ctypes.c_int64), ("my_substeps", ctypes.c_int64),
+                ("slab_z0", ctypes.c_int64), ("slab_nz", ctypes.c_int64),
+                ("points", ctypes.c_int64), ("macro_steps_done", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("t", ctypes.c_double),
+                ("bytes_per_point_substep", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class GbsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{msg} (code {code})")
+        self.code = code
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = False):
+    """Load libgbs_b200.so (in-tree).  Raises if it is missing — no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.LIB):
+        if build_if_missing:
+            _build.build()
+        else:
+            raise ImportError(f"{_build.LIB} is missing: run `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (nvcc sm_100a) first")
+    L = ctypes.CDLL(_build.LIB)
+    vp, i64, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)
+    L.gbs_create.argtypes = [ctypes.POINTER(gbs_grid), ctypes.c_int, ctypes.c_int,
+                             ctypes.POINTER(ctypes.c_int32), dp, ctypes.POINTER(gbs_dist), vp,
+                             ctypes.POINTER(vp)]
+    L.gbs_write_state.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_advance.argtypes = [vp, i64, ctypes.c_double]
+    L.gbs_read_state.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_sync.argtypes = [vp]
+    L.gbs_destroy.argtypes = [vp]
+    L.gbs_destroy.restype = None
+    L.gbs_nccl_unique_id.argtypes = [vp]
+    L.gbs_query.argtypes = [vp, ctypes.POINTER(gbs_info)]
+    L.gbs_set_option.argtypes = [vp, ctypes.c_char_p, i64]
+    L.gbs_kernel_time.argtypes = [vp, ctypes.c_int, dp, ctypes.POINTER(i64), ctypes.c_int]
+    L.gbs_strerror.argtypes = [ctypes.c_int]
+    L.gbs_strerror.restype = ctypes.c_char_p
+    L.gbs_last_error.argtypes = [vp]
+    L.gbs_last_error.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("gbs_destroy", "gbs_strerror", "gbs_last_error"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int, ctx=None):
+    if rc != GBS_OK:
+        L = load()
+        msg = L.gbs_last_error(ctx).decode() or L.gbs_strerror(rc).decode()
+        raise GbsError(rc, msg)
+
+
+def _ptr_and_device(buf):
+    """(address, on_device, n_values) of a torch tensor or numpy array of float64."""
+    if isinstance(buf, np.ndarray):
+        if buf.dtype != np.float64 or not buf.flags.c_contiguous:
+            raise TypeError("host buffers must be C-contiguous float64")
+        return buf.ctypes.data, 0, buf.size
+    import torch
+    if not isinstance(buf, torch.Tensor):
+        raise TypeError("buffer must be a numpy array or a torch tensor")
+    if buf.dtype != torch.float64 or not buf.is_contiguous():
+        raise TypeError("tensors must be contiguous float64")
+    return buf.data_ptr(), int(buf.is_cuda), buf.numel()
+
+
+# ---- same names as the C ABI ------------------------------------------------
+def gbs_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(load().gbs_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
+def gbs_create(pde: str, n: Sequence[int], stencil_order: int, n_k: Sequence[int],
+               w_k: Sequence[float], dist: Optional[dict] = None, stream=None,
+               length: Sequence[float] = (1.0, 1.0, 1.0)):
+    L = load()
+    g = gbs_grid()
+    g.pde = PDE[pde]
+    g.ndim = NDIM[pde]
+    for d in range(3):
+        g.n[d] = int(n[d]) if d < len(n) else 1
+        g.length[d] = float(length[d])
+    nk = (ctypes.c_int32 * len(n_k))(*[int(x) for x in n_k])
+    wk = (ctypes.c_double * len(w_k))(*[float(x) for x in w_k])
+    dp = None
+    if dist is not None:
+        dd = gbs_dist()
+        dd.rank, dd.world = int(dist["rank"]), int(dist["world"])
+        dd.device, dd.groups = int(dist.get("device", 0)), int(dist.get("groups", 0))
+        ctypes.memmove(dd.nccl_id, bytes(dist["nccl_id"]), 128)
+        dp = ctypes.pointer(dd)
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+    out = ctypes.c_void_p()
+    _check(L.gbs_create(ctypes.byref(g), int(stencil_order), len(n_k), nk, wk, dp,
+                        ctypes.c_void_p(int(stream) if stream else 0), ctypes.byref(out)))
+    return out
+
+
+def gbs_write_state(ctx, src) -> None:
+    p, dev, cnt = _ptr_and_device(src)
+    _check(load().gbs_write_state(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
+
+
+def gbs_advance(ctx, macro_steps: int, H: float) -> None:
+    _check(load().gbs_advance(ctx, int(macro_steps), float(H)), ctx)
+
+
+def gbs_read_state(ctx, dst) -> None:
+    p, dev, cnt = _ptr_and_device(dst)
+    _check(load().gbs_read_state(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
+
+
+def gbs_sync(ctx) -> None:
+    _check(load().gbs_sync(ctx), ctx)
+
+
+def gbs_destroy(ctx) -> None:
+    if ctx:
+        load().gbs_destroy(ctx)
+
+
+def gbs_query(ctx) -> dict:
+    info = gbs_info()
+    _check(load().gbs_query(ctx, ctypes.byref(info)), ctx)
+    return info.as_dict()
+
+
+def gbs_set_option(ctx, key: str, value: int) -> None:
+    _check(load().gbs_set_option(ctx, key.encode(), int(value)), ctx)
+
+
+def gbs_kernel_time(ctx, cls: int, reset: bool = False):
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(load().gbs_kernel_time(ctx, int(cls), ctypes.byref(ms), ctypes.byref(n), int(reset)), ctx)
+    return ms.value, n.value
+
+
+def gbs_strerror(code: int) -> str:
+    return load().gbs_strerror(int(code)).decode()
+
+
+def gbs_last_error(ctx=None) -> str:
+    return load().gbs_last_error(ctx).decode()
+
+
+class Stepper:
+    """RAII convenience around one context (still only marshalling)."""
+
+    def __init__(self, pde, n, stencil_order, n_k, w_k, dist=None, stream=None, **opts):
+        self.pde = pde
+        self.ctx = gbs_create(pde, n, stencil_order, n_k, w_k, dist, stream)
+        for k, v in opts.items():
+            gbs_set_option(self.ctx, k, v)
+
+    def write(self, y):
+        gbs_write_state(self.ctx, y)
+
+    def advance(self, macro_steps, H):
+        gbs_advance(self.ctx, macro_steps, H)
+
+    def read(self, out):
+        gbs_read_state(self.ctx, out)
+        return out
+
+    def info(self):
+        return gbs_query(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            gbs_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

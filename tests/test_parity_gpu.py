@@ -1,0 +1,308 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element,
+on the same seeded inputs.  Bar: max relative L2 <= 1e-12 in fp64 (BASELINE.json
+north_star), per field and over all fields.  Weights and H are the oracle's.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from gbs_inputs import get_config, make_ic, reduced
+from oracle import c_oracle as C
+from oracle import stability as S
+from oracle import weights as W
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1907_11771_b200 import gbs
+    gbs.load()
+    return torch
+
+
+def gbs_mod():
+    from paper_1907_11771_b200 import gbs
+    return gbs
+
+
+def rel_l2(a, b):
+    d = np.linalg.norm((a - b).ravel())
+    n = np.linalg.norm(b.ravel())
+    return float(d / n) if n > 0 else float(d)
+
+
+def assert_parity(got, ref, tol=TOL, what=""):
+    errs = [rel_l2(got[f], ref[f]) for f in range(ref.shape[0]) if np.linalg.norm(ref[f]) > 0]
+    errs.append(rel_l2(got, ref))
+    assert max(errs) <= tol, f"{what}: rel L2 per field/all = {errs}"
+    for f in range(ref.shape[0]):
+        if np.linalg.norm(ref[f]) == 0:
+            assert np.max(np.abs(got[f])) <= tol * max(1.0, np.linalg.norm(ref) / np.sqrt(ref.size))
+
+
+def scheme_for(w, wset=None):
+    counts, ws, _ = W.scheme(wset or w.weights, w.steps)
+    wd = W.to_double(ws)
+    H = S.macro_step_H(w.pde, w.order, w.n, counts, wd, w.h_factor)
+    if wset and wset != w.weights:
+        # parity-only sets use min(H_config, 0.5 ISB(set)/rho) (reading R7)
+        c0, w0, _ = W.scheme(w.weights, w.steps)
+        H = min(H, S.macro_step_H(w.pde, w.order, w.n, c0, W.to_double(w0), w.h_factor))
+    return counts, wd, H
+
+
+def run_gpu(torch, w, counts, wd, H, M, checkpoints=False, opts=None, host=False):
+    gbs = gbs_mod()
+    y0 = make_ic(w)
+    outs = []
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd, **(opts or {})) as st:
+        if host:
+            st.write(y0)
+        else:
+            st.write(torch.from_numpy(y0).cuda())
+        steps = [1] * M if checkpoints else [M]
+        for k in steps:
+            st.advance(k, H)
+            if host:
+                o = np.empty_like(y0)
+                st.read(o)
+                outs.append(o)
+            else:
+                o = torch.empty(y0.shape, dtype=torch.float64, device="cuda")
+                st.read(o)
+                outs.append(o.cpu().numpy())
+        info = st.info()
+    return y0, outs, info
+
+
+def run_oracle(w, y0, counts, wd, H, M, checkpoints=False):
+    if not checkpoints:
+        return [C.advance(w.pde, w.order, y0, counts, wd, H, M)]
+    outs, y = [], y0
+    for _ in range(M):
+        y = C.advance(w.pde, w.order, y, counts, wd, H, 1)
+        outs.append(y)
+    return outs
+
+
+# ----------------------------------------------------------------------------- C1 full size
+def test_c1_full_every_macro_step(torch_cuda):
+    w = get_config("c1")
+    counts, wd, H = scheme_for(w)
+    y0, g, info = run_gpu(torch_cuda, w, counts, wd, H, w.macro_steps, checkpoints=True)
+    o = run_oracle(w, y0, counts, wd, H, w.macro_steps, checkpoints=True)
+    for i, (a, b) in enumerate(zip(g, o)):
+        assert_parity(a, b, what=f"c1 macro step {i + 1}")
+    assert info["substeps_per_macro"] == 24
+
+
+# ----------------------------------------------------------------------------- reduced, ragged
+CASES = [
+    # (config, grid (nx, ny, nz), macro steps, weight set)
+    ("c1", (200, 1, 1), 20, "square8"),
+    ("c1", (77, 1, 1), 10, "square8"),             # odd, single ragged tile
+    ("c2", (200, 136, 1), 5, "fallback8"),         # ragged in x (256-wide tiles) and y
+    ("c2", (200, 136, 1), 5, "nonzero8"),
+    ("c2", (131, 90, 1), 3, "nonzero8"),           # odd nx -> 64-bit path
+    ("c3", (264, 200, 1), 3, "nonzero8"),
+    ("c3", (520, 72, 1), 2, "fallback8"),
+    ("c4", (72, 40, 36), 2, "nonzero8"),           # ragged: 64-wide x tiles, 16-high y tiles
+    ("c4", (72, 40, 36), 2, "fallback8"),
+    ("c4", (65, 33, 40), 1, "nonzero8"),           # odd nx -> 64-bit path
+    ("c5", (70, 34, 48), 1, "nonzero8"),           # {2..16}
+]
+
+
+@pytest.mark.parametrize("cfg,n,M,wset", CASES)
+def test_reduced_every_macro_step(torch_cuda, cfg, n, M, wset):
+    w = reduced(cfg, n, macro_steps=M, weights=wset)
+    counts, wd, H = scheme_for(w, wset)
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, M, checkpoints=True)
+    o = run_oracle(w, y0, counts, wd, H, M, checkpoints=True)
+    for i, (a, b) in enumerate(zip(g, o)):
+        assert_parity(a, b, what=f"{cfg} {n} {wset} macro step {i + 1}")
+
+
+# ----------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("cfg,n,order", [("c4", (9, 9, 9), 8), ("c2", (5, 5, 1), 4),
+                                         ("c3", (9, 9, 1), 8), ("c1", (5, 1, 1), 4)])
+def test_minimum_grid(torch_cuda, cfg, n, order):
+    w = reduced(cfg, n, macro_steps=2).with_(order=order)
+    counts, wd, H = scheme_for(w)
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, 2)
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(g[0], o[0], what=f"min grid {n}")
+
+
+def test_single_sequence_and_fd4_wave(torch_cuda):
+    w = reduced("c4", (24, 20, 18), macro_steps=3).with_(order=4, steps=(2,))
+    y0 = make_ic(w)
+    H = 1e-3
+    _, g, _ = run_gpu(torch_cuda, w, [2], [1.0], H, 3)
+    o = run_oracle(w, y0, [2], [1.0], H, 3)
+    assert_parity(g[0], o[0], what="m=1")
+
+
+def test_paper_scheme_gbs86(torch_cuda):
+    """GBS_8,6, 11 sequences, on a 3-D wave grid."""
+    w = reduced("c4", (34, 30, 28), macro_steps=2).with_(steps=tuple(range(2, 23, 2)),
+                                                          weights="GBS_8_6")
+    counts, ws, _ = W.scheme("GBS_8_6")
+    wd = W.to_double(ws)
+    H = S.macro_step_H(w.pde, w.order, w.n, counts, wd)
+    y0, g, info = run_gpu(torch_cuda, w, counts, wd, H, 2)
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(g[0], o[0], what="GBS_8_6")
+    assert info["substeps_per_macro"] == sum(n + 1 for n in counts)
+
+
+def test_host_buffers_match_device_buffers(torch_cuda):
+    w = reduced("c2", (96, 64, 1), macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, gd, _ = run_gpu(torch_cuda, w, counts, wd, H, 2)
+    _, gh, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, host=True)
+    assert np.array_equal(gd[0], gh[0])
+
+
+def test_graph_replay_is_bitwise_identical(torch_cuda):
+    w = reduced("c4", (40, 36, 34), macro_steps=3, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 3, opts={"graph": 1})
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 3, opts={"graph": 0})
+    assert ia["uses_graph"] == 1 and ib["uses_graph"] == 0
+    assert np.array_equal(a[0], b[0])
+    assert ia["kernel_launches"] == ib["kernel_launches"] == 3 * 48
+
+
+@pytest.mark.parametrize("cfg,n,slabs", [("c4", (40, 36, 32), 2), ("c4", (40, 36, 32), 4),
+                                         ("c5", (36, 20, 24), 3), ("c2", (96, 64, 1), 4),
+                                         ("c3", (80, 48, 1), 3)])
+def test_loopback_slabs(torch_cuda, cfg, n, slabs):
+    """z-slabs (y in 2-D) with ghost planes and halo copies, emulated on one GPU."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, g, info = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs})
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert info["slabs"] == slabs
+    assert_parity(g[0], o[0], what=f"loopback {slabs}")
+
+
+# ----------------------------------------------------------------------------- errors
+def test_error_paths(torch_cuda):
+    gbs = gbs_mod()
+    ctx = gbs.gbs_create("wave3d", (16, 16, 16), 8, [2, 4], [-1 / 3, 4 / 3])
+    try:
+        with pytest.raises(gbs.GbsError) as e:
+            gbs.gbs_advance(ctx, 1, 1e-3)
+        assert e.value.code == gbs.GBS_E_STATE
+        y = torch_cuda.zeros((2, 16, 16, 16), dtype=torch_cuda.float64, device="cuda")
+        gbs.gbs_write_state(ctx, y)
+        for H in (0.0, -1.0, float("inf"), float("nan")):
+            with pytest.raises(gbs.GbsError) as e:
+                gbs.gbs_advance(ctx, 1, H)
+            assert e.value.code == gbs.GBS_E_INVAL
+        with pytest.raises(gbs.GbsError) as e:
+            gbs.gbs_read_state(ctx, torch_cuda.zeros(10, dtype=torch_cuda.float64, device="cuda"))
+        assert e.value.code == gbs.GBS_E_INVAL
+        with pytest.raises(gbs.GbsError):
+            gbs.gbs_set_option(ctx, "no_such_option", 1)
+    finally:
+        gbs.gbs_destroy(ctx)
+
+
+def test_instability_is_reported(torch_cuda):
+    """H far beyond the ISB: the extreme mode overflows and GBS_E_NONFINITE surfaces."""
+    gbs = gbs_mod()
+    n = 16
+    x = np.arange(n) / n
+    z, yy, xx = np.meshgrid(x, x, x, indexing="ij")
+    u = np.cos(np.pi * n * xx) * np.cos(np.pi * n * yy) * np.cos(np.pi * n * z)
+    y0 = np.stack([u, np.zeros_like(u)])
+    counts, ws, _ = W.scheme("square8")
+    wd = W.to_double(ws)
+    H = 3.0 * S.isb(counts, wd) / S.rho("wave3d", 8, (n, n, n))
+    with gbs.Stepper("wave3d", (n, n, n), 8, counts, wd) as st:
+        st.write(torch_cuda.from_numpy(y0).cuda())
+        st.advance(400, H)
+        with pytest.raises(gbs.GbsError) as e:
+            st.read(torch_cuda.empty((2, n, n, n), dtype=torch_cuda.float64, device="cuda"))
+        assert e.value.code == gbs.GBS_E_NONFINITE
+
+
+# ----------------------------------------------------------------------------- full sizes
+def _sample_boxes(w, y0, counts, wd, H, centres):
+    """Oracle values at sampled points after ONE macro step, each from a periodically
+    extracted box of half-width r*(max n_k + 1) (bitwise equal to the full-grid oracle,
+    tests/test_oracle_stepping.py::test_box_sample_reproduces_full_grid_value_bitwise)."""
+    R = (w.order // 2) * (max(counts) + 1)
+    nx, ny, nz = w.n
+    vals = []
+    for c in centres:
+        if w.ndim == 3:
+            cz, cy, cx = c
+            iz = np.arange(cz - R, cz + R + 1) % nz
+            iy = np.arange(cy - R, cy + R + 1) % ny
+            ix = np.arange(cx - R, cx + R + 1) % nx
+            box = np.ascontiguousarray(y0[:, iz][:, :, iy][:, :, :, ix])
+            out = C.advance(w.pde, w.order, box, counts, wd, H, 1, scale=w.n)
+            vals.append(out[:, R, R, R])
+        else:
+            cy, cx = c
+            iy = np.arange(cy - R, cy + R + 1) % ny
+            ix = np.arange(cx - R, cx + R + 1) % nx
+            box = np.ascontiguousarray(y0[:, iy][:, :, ix])
+            out = C.advance(w.pde, w.order, box, counts, wd, H, 1, scale=w.n)
+            vals.append(out[:, R, R])
+    return np.array(vals)
+
+
+@pytest.mark.slow
+def test_c2_full_size(torch_cuda):
+    w = get_config("c2")
+    counts, wd, H = scheme_for(w)
+    M = 10
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, M)
+    o = run_oracle(w, y0, counts, wd, H, M)
+    assert_parity(g[0], o[0], what="c2 full, 10 macro steps")
+
+
+@pytest.mark.slow
+def test_c3_full_size(torch_cuda):
+    w = get_config("c3")
+    counts, wd, H = scheme_for(w)
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, 1)
+    o = run_oracle(w, y0, counts, wd, H, 1)
+    assert_parity(g[0], o[0], what="c3 full, 1 macro step")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_3d_full_size_sampled(torch_cuda, cfg):
+    torch = torch_cuda
+    gbs = gbs_mod()
+    w = get_config(cfg)
+    counts, wd, H = scheme_for(w)
+    y0 = make_ic(w)
+    nx, ny, nz = w.n
+    rng = np.random.default_rng(7)
+    centres = [(0, 0, 0), (nz - 1, ny - 1, nx - 1), (nz // 2, 0, nx - 1), (3, ny // 3, 5)]
+    centres += [tuple(int(v) for v in rng.integers(0, [nz, ny, nx])) for _ in range(4)]
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch.from_numpy(y0).cuda())
+        st.advance(1, H)
+        out = torch.empty(y0.shape, dtype=torch.float64, device="cuda")
+        st.read(out)
+        idx = torch.tensor(centres, device="cuda")
+        got = out[:, idx[:, 0], idx[:, 1], idx[:, 2]].T.cpu().numpy()
+        del out
+    ref = _sample_boxes(w, y0, counts, wd, H, centres)
+    scale = np.sqrt(np.mean(y0 * y0))          # RMS of the input (|R| <= 1: norms do not grow)
+    err = np.max(np.abs(got - ref)) / scale
+    assert err <= TOL, f"{cfg}: max |gpu - oracle| / rms = {err:.3e}"
