@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the GBS hot path (BASELINE.json metric: grid-point leap-frog substeps/s and
+% of HBM roofline at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One "step" = one macro step of the whole hot path (every FE / LF / final substep of every
+sequence, the weighted extrapolation and, for N > 1, the cross-GPU combine) over the
+workload's full grid.  Default workload: BASELINE.json configs[4] (C5, 3-D scalar wave 1024^3,
+FD8, step counts {2..16}, fallback order-8 weights; the metric's 1/2/4/8-GPU config), which
+fits one B200 (4 state buffers x 16 GiB).  value = grid points x S x K / max-over-ranks
+device time, S = sum_k (n_k + 1) substeps per macro step.
+
+--impl reference times the oracle (oracle/gbs_oracle.c, plain fp64 C, OpenMP over the
+outer grid loop) on this host's cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-point leap-frog substeps/sec and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "grid-point-substeps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--groups", type=int, default=0, help="sequence groups (0 = planner)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload_and_scheme(name):
+    from gbs_inputs import get_config
+    from paper_1907_11771_b200 import scheme
+    w = get_config(name)
+    counts, ws, _ = scheme.weight_set(w.weights, w.steps)
+    wd = scheme.to_fp64(ws)
+    H = scheme.macro_step(w.pde, w.order, w.n, counts, wd, w.h_factor)
+    return w, counts, wd, H
+
+
+def describe(w, H):
+    pde = {"adv1d": "1-D advection", "acoustic2d": "2-D acoustics", "wave3d": "3-D scalar wave"}[w.pde]
+    grid = "x".join(str(v) for v in w.n[: w.ndim])
+    return (f"{w.name}: {pde} {grid}, FD{w.order}, step counts {{{','.join(map(str, w.steps))}}} "
+            f"({w.weights} weights), H={H:.6g}, seeded {w.ic} IC")
+
+
+# ------------------------------------------------------------------------------ oracle timing
+def time_oracle_sample(w, counts, wd, H, target=1.0e9):
+    """The oracle, as it stands, on a bounded sample of workload w: one macro step on a
+    grid shrunk (same PDE, stencil, scheme, H, IC recipe) to ~1e9 pt-substeps."""
+    import numpy as np
+    from gbs_inputs import make_ic, reduced
+    from oracle import c_oracle
+    S = sum(n + 1 for n in counts)
+    pts = max(1, int(target / S))
+    if w.ndim == 3:
+        e = max(16, int(round(pts ** (1 / 3) / 16)) * 16)
+        n = (min(e, w.n[0]), min(e, w.n[1]), min(e, w.n[2]))
+    elif w.ndim == 2:
+        e = max(32, int(round(pts ** 0.5 / 32)) * 32)
+        n = (min(e, w.n[0]), min(e, w.n[1]), 1)
+    else:
+        n = w.n
+    ws = reduced(w.name, n, macro_steps=1)
+    y0 = make_ic(ws)
+    cores = os.cpu_count() or 1
+    c_oracle.set_threads(cores)
+    macro = 1 if w.ndim > 1 else 20
+    t0 = time.perf_counter()
+    c_oracle.advance(ws.pde, ws.order, y0, counts, wd, H, macro, scale=w.n)
+    dt = time.perf_counter() - t0
+    units = ws.points * S * macro
+    grid = "x".join(str(v) for v in n[: w.ndim])
+    return {"value": units / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{macro} macro step(s) of the {w.name} scheme (same PDE, FD{w.order}, steps, "
+                      f"weights, H) on a {grid} grid = {units:.3g} pt-substeps in {dt:.2f} s"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w, counts, wd, H = workload_and_scheme(a.config)
+    for _ in range(max(0, a.warmup)):
+        time_oracle_sample(w, counts, wd, H, target=1e8)
+    vals = []
+    samples = []
+    for _ in range(max(1, a.steps)):
+        r = time_oracle_sample(w, counts, wd, H)
+        vals.append(r["value"])
+        samples.append(r)
+    v = statistics.median(vals)
+    cb = dict(samples[0])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": describe(w, H), "sample": cb["sample"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from gbs_inputs import make_ic
+    from paper_1907_11771_b200 import gbs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, counts, wd, H = workload_and_scheme(a.config)
+    y0 = make_ic(w)                                   # host IC (same recipe as the oracle's)
+    stream = torch.cuda.Stream()
+    dist_desc = None
+    if world > 1:
+        obj = [gbs.gbs_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        dist_desc = {"rank": rank, "world": world, "device": local, "groups": a.groups,
+                     "nccl_id": obj[0]}
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with torch.cuda.stream(stream):
+        st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream)
+        y0_dev = torch.from_numpy(y0).to("cuda", non_blocking=False)
+        st.write(y0_dev)
+        gbs.gbs_sync(st.ctx)
+        del y0_dev
+        info = st.info()
+        # warm-up (also builds the CUDA graph when one is used)
+        st.advance(a.warmup, H)
+        gbs.gbs_sync(st.ctx)
+        # timed region: per-kernel CUDA events on the context stream (time_kernels)
+        gbs.gbs_set_option(st.ctx, "time_kernels", 1)
+        gbs.gbs_kernel_time(st.ctx, 0, reset=True)
+        gbs.gbs_kernel_time(st.ctx, 1, reset=True)
+        gbs.gbs_kernel_time(st.ctx, 2, reset=True)
+        l0 = st.info()["kernel_launches"]
+        clk = ClockSampler(local)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        clk.start()
+        e0.record(stream)
+        st.advance(a.steps, H)
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+        clocks = clk.stop()
+        gbs.gbs_sync(st.ctx)
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        launches = st.info()["kernel_launches"] - l0
+        lf_ms, lf_n = gbs.gbs_kernel_time(st.ctx, 0)
+        fe_ms, fe_n = gbs.gbs_kernel_time(st.ctx, 1)
+        fin_ms, fin_n = gbs.gbs_kernel_time(st.ctx, 2)
+        gbs.gbs_set_option(st.ctx, "time_kernels", 0)
+
+    S = info["substeps_per_macro"]
+    units = w.points * S * a.steps
+    value = units / (ms * 1e-3)
+    F = w.fields
+    local_pts = w.points // max(1, info["slabs"])
+    peak, peak_src = peaks()
+    lf_avg = lf_ms / max(lf_n, 1)
+    achieved = 24.0 * F * local_pts / (lf_avg * 1e-3) / 1e9          # GB/s, algorithmic
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("config") == w.name:
+            traffic = tr.get("lf_dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "interior leap-frog substep (TMA-pipelined z-march)",
+                "algorithmic_bytes_per_launch": 24 * F * local_pts,
+                "avg_launch_ms": round(lf_avg, 4), "peak_source": peak_src,
+                "share_of_step": round(lf_ms / ms, 4) if ms > 0 else None,
+                "other_kernels": {
+                    "fe_avg_ms": round(fe_ms / max(fe_n, 1), 4), "fe_GBps_alg": round(
+                        16.0 * F * local_pts / (fe_ms / max(fe_n, 1) * 1e-3) / 1e9, 1) if fe_n else None,
+                    "final_avg_ms": round(fin_ms / max(fin_n, 1), 4), "final_GBps_alg": round(
+                        24.0 * F * local_pts / (fin_ms / max(fin_n, 1) * 1e-3) / 1e9, 1) if fin_n else None}}
+
+    # ---- end to end through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if a.e2e_steps > 0:
+        with torch.cuda.stream(stream):
+            h_in = torch.from_numpy(y0).pin_memory()
+            h_out = torch.empty(y0.shape, dtype=torch.float64).pin_memory()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(a.e2e_steps):
+                gbs.gbs_write_state(st.ctx, h_in)
+                gbs.gbs_advance(st.ctx, 1, H)
+                gbs.gbs_read_state(st.ctx, h_out)          # synchronizes
+            barrier()
+            dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": w.points * S * a.e2e_steps / dt, "unit": UNIT, "steps": a.e2e_steps,
+               "h2d_bytes_per_step": int(y0.nbytes), "d2h_bytes_per_step": int(y0.nbytes),
+               "note": "gbs_write_state(pinned host) + gbs_advance(1 macro step) + gbs_read_state(pinned host)"}
+        del h_in, h_out
+    st.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = time_oracle_sample(w, counts, wd, H)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": describe(w, H), "grid": list(w.n[: w.ndim]), "fields": F,
+                           "substeps_per_step": S, "step": "1 macro step (all sequences + combine)",
+                           "l2": "inputs larger than L2 (each state buffer %.1f GiB)" % (y0.nbytes / 2 ** 30),
+                           "plan": {"groups": info["groups"], "slabs": info["slabs"]},
+                           "hbm_roofline_fraction_of_step": round(
+                               value * 24 * F / (peak * 1e9 * world), 4)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -16,6 +16,7 @@
 // local slabs in loopback mode, ncclSend/ncclRecv between ranks).
 #include "gbs.h"
 #include "gbs_kernels.cuh"
+#include "gbs_wave3d_tma.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -77,7 +78,40 @@ static Api& api() {
 struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
     double* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // Y, ACC, B, C (+ ghosts)
+    bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
+    CUtensorMap tm[4][2][3];          // [buffer][field][box shape A/B/C] (wave3d)
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled_t encode_tiled() {
+    static EncodeTiled_t fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiled_t)p;
+    }
+    return fn;
+}
+
+// 3-D fp64 view [dz][ny][nx] at base with box (bx, by, 1)
+static bool make_map(CUtensorMap* m, double* base, int64_t nx, int64_t ny, int64_t dz, int bx, int by) {
+    EncodeTiled_t enc = encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)dz};
+    cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)(nx * ny) * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 struct KernelTimer {
     std::vector<cudaEvent_t> ev;      // pairs
@@ -116,6 +150,7 @@ struct gbs_ctx {
     bool have_state = false;
     bool use_graph = true;
     bool time_kernels = false;
+    bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
     int zchunk_opt = 0;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     double graph_H = -1.0;
@@ -263,6 +298,20 @@ static int alloc_state(gbs_ctx* c) {
                 return fail(c, GBS_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
             CU(c, cudaMemsetAsync(s.buf[b], 0, bytes, c->stream));
         }
+        // TMA kernels: the grid must be a multiple of the tile so halo boxes never cross the wrap
+        s.tma_ok = false;
+        if (c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0) {
+            bool ok = true;
+            const int64_t dz = nzl + 2 * c->ghost;
+            for (int b = 0; b < 4 && ok; ++b)
+                for (int f = 0; f < 2 && ok; ++f) {
+                    double* base = s.buf[b] + (int64_t)f * c->field_stride;
+                    ok = make_map(&s.tm[b][f][0], base, c->n[0], c->n[1], dz, gbs::tma::TX, gbs::tma::TY) &&
+                         make_map(&s.tm[b][f][1], base, c->n[0], c->n[1], dz, gbs::tma::TX, c->R) &&
+                         make_map(&s.tm[b][f][2], base, c->n[0], c->n[1], dz, c->R, gbs::tma::TY);
+                }
+            s.tma_ok = ok;
+        }
     }
     CU(c, cudaMalloc(&c->d_flag, sizeof(int)));
     CU(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
@@ -290,6 +339,20 @@ template <int R, int MODE, bool SLAB>
 static void launch_wave3d(const gbs::Wave3DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
     if (vx2) gbs::wave3d_step<R, MODE, 2, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
     else gbs::wave3d_step<R, MODE, 1, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
+}
+template <int R, int MODE, bool SLAB>
+static cudaError_t launch_wave3d_tma(const gbs::tma::Maps& m, const gbs::Wave3DArgs& a, int zbase, dim3 grid,
+                                     cudaStream_t st) {
+    using L = gbs::tma::Layout<R, MODE>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::wave3d_step_tma<R, MODE, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gbs::tma::wave3d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, zbase);
+    return cudaSuccess;
 }
 template <int R, int MODE, bool SLAB>
 static void launch_ac2d(const gbs::Acoustic2DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
@@ -321,6 +384,34 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
         a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
         const bool vx2 = (c->n[0] % 2) == 0;
+        if (c->use_bulk && s.tma_ok) {
+            int64_t tx = c->n[0] / gbs::tma::TX, ty = c->n[1] / gbs::tma::TY;
+            a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, s.nz)
+                                         : (int)std::min<int64_t>(128, s.nz);
+            dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
+            gbs::tma::Maps m;
+            m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
+            m.sv = s.tm[op.S][1][0];
+            m.pu = s.tm[op.P][0][0]; m.pv = s.tm[op.P][1][0];
+            m.au = s.tm[op.O][0][0]; m.av = s.tm[op.O][1][0];
+            const int zbase = (int)c->ghost;
+            cudaError_t e = cudaSuccess;
+#define W3B(RR, SL)                                                                                   \
+            switch (op.mode) {                                                                        \
+                case gbs::MODE_FE: e = launch_wave3d_tma<RR, gbs::MODE_FE, SL>(m, a, zbase, grid, c->stream); break;     \
+                case gbs::MODE_LF: e = launch_wave3d_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream); break;     \
+                case gbs::MODE_FIN0: e = launch_wave3d_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break; \
+                default: e = launch_wave3d_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;           \
+            }
+            if (c->R == 2) { if (slab) { W3B(2, true) } else { W3B(2, false) } }
+            else { if (slab) { W3B(4, true) } else { W3B(4, false) } }
+#undef W3B
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "bulk kernel setup: %s", cudaGetErrorString(e));
+            c->launches++;
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return GBS_OK;
+        }
         const int TX = vx2 ? 64 : 32, TY = 16;
         int64_t tx = (c->n[0] + TX - 1) / TX, ty = (c->n[1] + TY - 1) / TY;
         a.zchunk = chunk_for(tx * ty, s.nz, c->zchunk_opt);
@@ -710,6 +801,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "graph") { c->use_graph = value != 0 && c->world == 1; drop_graphs(); return GBS_OK; }
     if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");
         if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback needs a single-GPU context");

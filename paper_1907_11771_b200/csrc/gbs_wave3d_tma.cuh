@@ -1,0 +1,263 @@
+// gbs_wave3d_tma.cuh -- 3-D wave substep kernel fed by the Tensor Memory
+// Accelerator (cp.async.bulk.tensor, SASS UTMALDG) through a D-stage
+// full/empty mbarrier pipeline with a dedicated producer warp.
+//
+// Same arithmetic, operand order and modes as gbs::wave3d_step
+// (gbs_kernels.cuh), so the two kernels agree bit for bit: one launch is one
+// FE / LF / final substep of one GBS sequence (Eq. (1), lines 85-98),
+// the FIN modes fused with the averaging and the weighted accumulate
+// (PAPER.md:109-115, 221-225).
+//
+// Why: the register-prefetch kernel keeps only about one plane of loads in
+// flight per SM (1 CTA x 512 threads at 128 registers), which caps it near 78%
+// of the copy bandwidth.  Here one producer thread issues 5 + NP tensor boxes
+// per plane, up to D planes ahead of the 16 consumer warps, so the bytes in
+// flight no longer depend on the register budget.
+//
+// Tile: TX = 64 (x) by TY = 16 (y) points, 16 consumer warps of 32 threads x 2
+// points + 1 producer warp.  Per plane the u tile is five boxes that never
+// overlap and never cross the periodic boundary (the grid is a multiple of the
+// tile, so a wrapped halo box is simply a box at the wrapped coordinate):
+//   centre column [TY + 2R][TX]: top halo (TX x R), centre (TX x TY), bottom halo (TX x R)
+//   x strips [TY][R]: left (R x TY at x0 - R), right (R x TY at x0 + TX)
+// Shared memory: ring[R + D] of those tiles (plane z is the x/y stencil at
+// iteration z and the register-queue front at iteration z - R) and pw[D][NP]
+// TX x TY tiles of the pointwise streams (v of the current level, u and v of
+// the previous level, the accumulator for FINACC).
+#pragma once
+
+#include <cuda.h>
+
+#include "gbs_kernels.cuh"
+
+namespace gbs {
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+template <int MODE> struct NPW { static constexpr int v = (MODE == MODE_FE) ? 1 : (MODE == MODE_FINACC ? 5 : 3); };
+template <int MODE> struct Depth { static constexpr int v = (MODE == MODE_FINACC) ? 3 : 4; };
+
+constexpr int TX = 64, TY = 16;
+
+template <int R, int MODE>
+struct Layout {
+    static constexpr int SH = TY + 2 * R;
+    static constexpr int D = Depth<MODE>::v;
+    static constexpr int RING = R + D;
+    static constexpr int NP = NPW<MODE>::v;
+    static constexpr int CENTER = SH * TX;                 // doubles of the centre column
+    static constexpr int STRIP = TY * R;                   // doubles of one x strip
+    static constexpr int TILE = CENTER + 2 * STRIP;        // doubles per u tile (128 B multiple)
+    static constexpr int PWT = TY * TX;
+    static constexpr size_t ring_doubles = (size_t)RING * TILE;
+    static constexpr size_t pw_doubles = (size_t)D * NP * PWT;
+    static constexpr size_t bytes = (ring_doubles + pw_doubles) * 8 + (2 * D + 1) * 8;
+    static constexpr uint32_t tile_bytes = TILE * 8;
+    static constexpr uint32_t stage_bytes = tile_bytes + NP * PWT * 8;
+    static_assert((CENTER * 8) % 128 == 0 && (STRIP * 8) % 128 == 0, "TMA destinations need 128 B alignment");
+};
+
+// Tensor maps of one launch.  Each map is a 3-D view [nz_alloc][ny][nx] of one
+// field buffer (ghost planes included in slab mode; z coordinate = z + zbase).
+struct Maps {
+    CUtensorMap su_a, su_b, su_c;      // u of the current level: TXxTY, TXxR, RxTY boxes
+    CUtensorMap sv, pu, pv, au, av;    // TXxTY boxes
+};
+
+template <int R, int MODE, bool SLAB>
+__global__ void __launch_bounds__(544, 1)
+wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zbase) {
+    using L = Layout<R, MODE>;
+    constexpr int D = L::D, RING = L::RING, NP = L::NP, TILE = L::TILE, PWT = L::PWT;
+    extern __shared__ __align__(128) double smem[];
+    double* ring = smem;
+    double* pw = smem + L::ring_doubles;
+    uint64_t* full = reinterpret_cast<uint64_t*>(pw + L::pw_doubles);
+    uint64_t* empty = full + D;
+    uint64_t* init = empty + D;
+
+    const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
+    const int nx = A.nx, ny = A.ny, nz = A.nz;
+    // x-tiles vary fastest in the launch order: resident CTAs stream whole rows
+    // (DRAM page locality; y-fastest order measured 10% slower on 1024^3)
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int z0 = blockIdx.z * A.zchunk;
+    const int niter = min(A.zchunk, nz - z0);
+
+    auto zc = [&](int z) -> int {              // tensor z coordinate of logical plane z
+        if constexpr (SLAB) return z + zbase;
+        else return wrap_once(z, nz);
+    };
+
+    if (ty == 0 && lane == 0) {
+        for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TY); }
+        mbar_init(init, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (ty == TY) {
+        // ===================== producer warp =====================
+        if (lane != 0) return;
+        prefetch_map(&M.su_a); prefetch_map(&M.su_b); prefetch_map(&M.su_c); prefetch_map(&M.sv);
+        if constexpr (MODE != MODE_FE) { prefetch_map(&M.pu); prefetch_map(&M.pv); }
+        if constexpr (MODE == MODE_FINACC) { prefetch_map(&M.au); prefetch_map(&M.av); }
+        const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
+        const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
+        auto issue_tile = [&](int p, uint64_t* bar) {
+            double* t = ring + (size_t)(p % RING) * TILE;
+            const int z = zc(z0 + p);
+            tma_load_3d(t, &M.su_b, x0, ytop, z, bar);
+            tma_load_3d(t + R * TX, &M.su_a, x0, y0, z, bar);
+            tma_load_3d(t + (R + TY) * TX, &M.su_b, x0, ybot, z, bar);
+            tma_load_3d(t + L::CENTER, &M.su_c, xl, y0, z, bar);
+            tma_load_3d(t + L::CENTER + L::STRIP, &M.su_c, xr, y0, z, bar);
+        };
+        mbar_expect_tx(init, R * L::tile_bytes);
+        for (int p = 0; p < R; ++p) issue_tile(p, init);
+        for (int i = 0; i < niter; ++i) {
+            const int s = i % D;
+            if (i >= D) mbar_wait(&empty[s], (uint32_t)(((i / D) - 1) & 1));
+            mbar_expect_tx(&full[s], L::stage_bytes);
+            issue_tile(i + R, &full[s]);
+            double* p = pw + (size_t)s * NP * PWT;
+            const int z = zc(z0 + i);
+            tma_load_3d(p, &M.sv, x0, y0, z, &full[s]);
+            if constexpr (MODE != MODE_FE) {
+                tma_load_3d(p + PWT, &M.pu, x0, y0, z, &full[s]);
+                tma_load_3d(p + 2 * PWT, &M.pv, x0, y0, z, &full[s]);
+            }
+            if constexpr (MODE == MODE_FINACC) {
+                tma_load_3d(p + 3 * PWT, &M.au, x0, y0, z, &full[s]);
+                tma_load_3d(p + 4 * PWT, &M.av, x0, y0, z, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ===================== consumer warps =====================
+    const int64_t plane = A.plane;
+    const int64_t own = (int64_t)(y0 + ty) * nx + x0 + 2 * tx;
+    auto zoff = [&](int z) -> int64_t {
+        if constexpr (SLAB) return (int64_t)z * plane;
+        else return (int64_t)wrap_once(z, nz) * plane;
+    };
+    using V = Vec<2>;
+    V q[2 * R + 1];
+#pragma unroll
+    for (int j = 0; j < R; ++j) q[j] = V::ld(A.Su + zoff(z0 - R + j) + own);   // planes z0-R .. z0-1
+    mbar_wait(init, 0);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const double2 t = *reinterpret_cast<const double2*>(ring + (size_t)j * TILE + (R + ty) * TX + 2 * tx);
+        q[R + j].v[0] = t.x; q[R + j].v[1] = t.y;
+    }
+
+    bool bad = false;
+    for (int i = 0; i < niter; ++i) {
+        const int s = i % D;
+        mbar_wait(&full[s], (uint32_t)((i / D) & 1));
+        const double* tile = ring + (size_t)(i % RING) * TILE;               // plane z
+        const double* front = ring + (size_t)((i + R) % RING) * TILE;        // plane z + R
+        {
+            const double2 f = *reinterpret_cast<const double2*>(front + (R + ty) * TX + 2 * tx);
+            q[2 * R].v[0] = f.x; q[2 * R].v[1] = f.y;
+        }
+        // x window: columns 2tx - R .. 2tx + R + 1 (pairs from the centre column or a strip)
+        double xw[2 * R + 2];
+#pragma unroll
+        for (int k = 0; k <= R; ++k) {
+            const int col = 2 * tx - R + 2 * k;
+            const double* src = col < 0 ? tile + L::CENTER + ty * R + (col + R)
+                              : col >= TX ? tile + L::CENTER + L::STRIP + ty * R + (col - TX)
+                                          : tile + (R + ty) * TX + col;
+            const double2 t = *reinterpret_cast<const double2*>(src);
+            xw[2 * k] = t.x; xw[2 * k + 1] = t.y;
+        }
+        const double* crow = tile + (R + ty) * TX + 2 * tx;
+        double lx[2], ly[2], lz[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const double c = xw[R + v];
+            lx[v] = FD<R>::b0() * c; ly[v] = FD<R>::b0() * c; lz[v] = FD<R>::b0() * c;
+        }
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            const double2 up = *reinterpret_cast<const double2*>(crow - j * TX);
+            const double2 dn = *reinterpret_cast<const double2*>(crow + j * TX);
+            const double upv[2] = {up.x, up.y}, dnv[2] = {dn.x, dn.y};
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                lx[v] = fma(FD<R>::b(j), xw[R + v + j] + xw[R + v - j], lx[v]);
+                ly[v] = fma(FD<R>::b(j), dnv[v] + upv[v], ly[v]);
+                lz[v] = fma(FD<R>::b(j), q[R + j].v[v] + q[R - j].v[v], lz[v]);
+            }
+        }
+        const double* pws = pw + (size_t)s * NP * PWT + ty * TX + 2 * tx;
+        const double2 sv = *reinterpret_cast<const double2*>(pws);
+        double2 pu = make_double2(0, 0), pv = make_double2(0, 0), au = make_double2(0, 0), av = make_double2(0, 0);
+        if constexpr (MODE != MODE_FE) {
+            pu = *reinterpret_cast<const double2*>(pws + PWT);
+            pv = *reinterpret_cast<const double2*>(pws + 2 * PWT);
+        }
+        if constexpr (MODE == MODE_FINACC) {
+            au = *reinterpret_cast<const double2*>(pws + 3 * PWT);
+            av = *reinterpret_cast<const double2*>(pws + 4 * PWT);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);          // this warp is done with stage s
+        const double svv[2] = {sv.x, sv.y}, puv[2] = {pu.x, pu.y}, pvv[2] = {pv.x, pv.y};
+        const double auv[2] = {au.x, au.y}, avv[2] = {av.x, av.y};
+        double ou[2], ov[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const double lap = fma(A.sx2, lx[v], fma(A.sy2, ly[v], A.sz2 * lz[v]));
+            ou[v] = combine<MODE>(puv[v], xw[R + v], svv[v], auv[v], A.cf, A.wh);
+            ov[v] = combine<MODE>(pvv[v], svv[v], lap, avv[v], A.cf, A.wh);
+            if constexpr (MODE == MODE_FIN0 || MODE == MODE_FINACC)
+                bad |= !isfinite(ou[v]) || !isfinite(ov[v]);
+        }
+        const int64_t o = zoff(z0 + i) + own;
+        *reinterpret_cast<double2*>(A.Ou + o) = make_double2(ou[0], ou[1]);
+        *reinterpret_cast<double2*>(A.Ov + o) = make_double2(ov[0], ov[1]);
+#pragma unroll
+        for (int j = 0; j < 2 * R; ++j) q[j] = q[j + 1];
+    }
+    if constexpr (MODE == MODE_FIN0 || MODE == MODE_FINACC)
+        if (bad && A.nonfinite) *A.nonfinite = 1;
+}
+
+}  // namespace tma
+}  // namespace gbs

@@ -117,7 +117,22 @@ CASES = [
     ("c4", (72, 40, 36), 2, "fallback8"),
     ("c4", (65, 33, 40), 1, "nonzero8"),           # odd nx -> 64-bit path
     ("c5", (70, 34, 48), 1, "nonzero8"),           # {2..16}
+    ("c4", (136, 40, 30), 2, "nonzero8"),          # bulk-copy kernel, ragged x tile + wrap split
+    ("c5", (128, 48, 36), 1, "nonzero8"),          # TMA kernel (multiple of the 64x16 tile)
+    ("c4", (64, 32, 20), 2, "fallback8"),          # TMA kernel, wrap on every halo box
 ]
+
+
+@pytest.mark.parametrize("n", [(128, 64, 64), (64, 16, 9), (192, 48, 40), (136, 40, 30)])
+def test_bulk_kernel_bitwise_equals_ldg_kernel(torch_cuda, n):
+    """The TMA-pipelined kernel (grids that are multiples of its 64x16 tile) and the
+    register-prefetch kernel do the same arithmetic in the same order: results must
+    agree bit for bit."""
+    w = reduced("c4", n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"bulk": 1})
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"bulk": 0})
+    assert np.array_equal(a[0], b[0])
 
 
 @pytest.mark.parametrize("cfg,n,M,wset", CASES)
@@ -182,6 +197,7 @@ def test_graph_replay_is_bitwise_identical(torch_cuda):
 
 
 @pytest.mark.parametrize("cfg,n,slabs", [("c4", (40, 36, 32), 2), ("c4", (40, 36, 32), 4),
+                                         ("c4", (128, 32, 36), 3),
                                          ("c5", (36, 20, 24), 3), ("c2", (96, 64, 1), 4),
                                          ("c3", (80, 48, 1), 3)])
 def test_loopback_slabs(torch_cuda, cfg, n, slabs):
