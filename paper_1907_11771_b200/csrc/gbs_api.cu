@@ -17,6 +17,7 @@
 #include "gbs.h"
 #include "gbs_kernels.cuh"
 #include "gbs_wave3d_tma.cuh"
+#include "gbs_wave3d_pair.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -77,9 +78,9 @@ static Api& api() {
 // ---------------------------------------------------------------------------
 struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
-    double* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // Y, ACC, B, C (+ ghosts)
+    double* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // Y, ACC, L0..L3 (+ ghosts)
     bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
-    CUtensorMap tm[4][2][3];          // [buffer][field][box shape A/B/C] (wave3d)
+    CUtensorMap tm[6][2][3];          // [buffer][field][box shape A/B/C] (wave3d)
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -117,8 +118,8 @@ struct KernelTimer {
     std::vector<cudaEvent_t> ev;      // pairs
     std::vector<int> cls;
     size_t used = 0;
-    double total_ms[3] = {0, 0, 0};
-    int64_t launches[3] = {0, 0, 0};
+    double total_ms[5] = {0, 0, 0, 0, 0};
+    int64_t launches[5] = {0, 0, 0, 0, 0};
 };
 
 struct gbs_ctx {
@@ -151,6 +152,10 @@ struct gbs_ctx {
     bool use_graph = true;
     bool time_kernels = false;
     bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
+    bool use_fuse = false;            // two-substep (temporally blocked) kernels where eligible
+                                      // (bit-exact, but latency-bound: off by default)
+    bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
+    int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     double graph_H = -1.0;
@@ -286,13 +291,17 @@ static int alloc_state(gbs_ctx* c) {
     int64_t nzl = c->nslow / total_slabs;
     c->ghost = total_slabs > 1 ? c->R : 0;
     c->field_stride = (nzl + 2 * c->ghost) * c->plane;
+    // the TMA (and two-substep) kernels need the grid to be a multiple of their tile so
+    // halo boxes never cross the wrap; the two-substep kernels need 4 level buffers
+    c->tma_grid = c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0;
+    c->nbuf = c->tma_grid ? 6 : 4;
     c->slab.resize(nloc);
     for (int v = 0; v < nloc; ++v) {
         Slab& s = c->slab[v];
         int64_t gidx = (int64_t)c->my_slab * nloc + v;
         s.z0 = gidx * nzl;
         s.nz = nzl;
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < c->nbuf; ++b) {
             size_t bytes = sizeof(double) * (size_t)c->F * (size_t)c->field_stride;
             if (cudaMalloc(&s.buf[b], bytes) != cudaSuccess)
                 return fail(c, GBS_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
@@ -300,10 +309,10 @@ static int alloc_state(gbs_ctx* c) {
         }
         // TMA kernels: the grid must be a multiple of the tile so halo boxes never cross the wrap
         s.tma_ok = false;
-        if (c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0) {
+        if (c->tma_grid) {
             bool ok = true;
             const int64_t dz = nzl + 2 * c->ghost;
-            for (int b = 0; b < 4 && ok; ++b)
+            for (int b = 0; b < c->nbuf && ok; ++b)
                 for (int f = 0; f < 2 && ok; ++f) {
                     double* base = s.buf[b] + (int64_t)f * c->field_stride;
                     ok = make_map(&s.tm[b][f][0], base, c->n[0], c->n[1], dz, gbs::tma::TX, gbs::tma::TY) &&
@@ -320,7 +329,7 @@ static int alloc_state(gbs_ctx* c) {
 
 static void free_state(gbs_ctx* c) {
     for (auto& s : c->slab)
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < 6; ++b)
             if (s.buf[b]) { cudaFree(s.buf[b]); s.buf[b] = nullptr; }
     c->slab.clear();
 }
@@ -352,6 +361,20 @@ static cudaError_t launch_wave3d_tma(const gbs::tma::Maps& m, const gbs::Wave3DA
         configured = true;
     }
     gbs::tma::wave3d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, zbase);
+    return cudaSuccess;
+}
+template <int R, int MODEB, bool SLAB>
+static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::PairArgs& a, int zbase, dim3 grid,
+                                   cudaStream_t st) {
+    using L = gbs::tma::PairLayout<R, MODEB>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::wave3d_pair_tma<R, MODEB, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY), L::bytes, st>>>(m, a, zbase);
     return cudaSuccess;
 }
 template <int R, int MODE, bool SLAB>
@@ -474,16 +497,72 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
     return GBS_OK;
 }
 
+// Two consecutive substeps of one sequence in one launch (3-D wave, TMA grids):
+// step A = LF from (P, S); step B = LF (writes OA = y_{n+1}, OB = y_{n+2}) or the
+// fused final step (modeB = FIN0/FINACC, writes the accumulator OB only).
+struct PairOperands {
+    int P, S, OA, OB;
+    int modeB;
+    double cfA, cfB, wh;
+    bool flag;
+};
+
+static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
+    const bool slab = c->ghost > 0;
+    gbs::tma::PairArgs a;
+    a.Au = field_ptr(c, s, op.OA, 0); a.Av = field_ptr(c, s, op.OA, 1);
+    a.Bu = field_ptr(c, s, op.OB, 0); a.Bv = field_ptr(c, s, op.OB, 1);
+    a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1); a.Pu = field_ptr(c, s, op.P, 0);
+    a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
+    a.plane = c->plane;
+    const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
+    a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
+    a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
+    a.nonfinite = op.flag ? c->d_flag : nullptr;
+    a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, s.nz) : (int)std::min<int64_t>(128, s.nz);
+    dim3 grid((unsigned)(c->n[0] / gbs::tma::TX), (unsigned)(c->n[1] / gbs::tma::TY),
+              (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
+    gbs::tma::PairMaps m;
+    m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
+    m.sv_a = s.tm[op.S][1][0]; m.sv_b = s.tm[op.S][1][1]; m.sv_c = s.tm[op.S][1][2];
+    m.pu_a = s.tm[op.P][0][0]; m.pu_b = s.tm[op.P][0][1]; m.pu_c = s.tm[op.P][0][2];
+    m.pv = s.tm[op.P][1][0];
+    m.acc_u = s.tm[op.OB][0][0]; m.acc_v = s.tm[op.OB][1][0];
+    const int zbase = (int)c->ghost;
+    cudaError_t e = cudaSuccess;
+#define PR(RR, SL)                                                                                          \
+    switch (op.modeB) {                                                                                     \
+        case gbs::MODE_LF: e = launch_pair_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream); break;     \
+        case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break; \
+        default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;           \
+    }
+    if (c->R == 2) { if (slab) { PR(2, true) } else { PR(2, false) } }
+    else { if (slab) { PR(4, true) } else { PR(4, false) } }
+#undef PR
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "pair kernel setup: %s", cudaGetErrorString(e));
+    c->launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
 // ---------------------------------------------------------------------------
-// halo exchange of buffer b's halo fields (ghost planes along the slowest axis)
+// halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
+// whose stencil crosses the slab axis) -- ghost planes along the slowest axis
 // ---------------------------------------------------------------------------
-static int exchange_halo(gbs_ctx* c, int b) {
+static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0) {
     if (c->ghost == 0) return GBS_OK;
     const int64_t G = c->ghost, P = c->plane;
     const size_t cnt = (size_t)(G * P);
     std::vector<int> fields;
-    if (c->pde == GBS_WAVE3D) fields = {0};
-    else fields = {0, 2};                       // acoustics: p and v cross the y slabs
+    if (mask) {
+        for (int f = 0; f < c->F; ++f)
+            if (mask & (1u << f)) fields.push_back(f);
+    } else if (c->pde == GBS_WAVE3D) {
+        fields = {0};
+    } else {
+        fields = {0, 2};                        // acoustics: p and v cross the y slabs
+    }
     const int nloc = c->loopback;
     const int S = c->slabs * nloc;              // global slab count
     if (c->slabs == 1) {
@@ -552,6 +631,26 @@ static int step(gbs_ctx* c, int cls, const StepOperands& op) {
     return GBS_OK;
 }
 
+static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
+    int rc;
+    // the pair kernel reads S_u, S_v and P_u with stencils
+    if ((rc = exchange_halo(c, op.S, 0x3u))) return rc;
+    if ((rc = exchange_halo(c, op.P, 0x1u))) return rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
+    for (auto& s : c->slab)
+        if ((rc = launch_pair(c, s, op))) return rc;
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    return GBS_OK;
+}
+
+static bool fused_path(const gbs_ctx* c) {
+    if (!(c->use_fuse && c->use_bulk && c->nbuf == 6)) return false;
+    for (const auto& s : c->slab)
+        if (!s.tma_ok) return false;
+    return true;
+}
+
 static int harvest_timer(gbs_ctx* c) {
     KernelTimer& T = c->timer;
     if (!T.used) return GBS_OK;
@@ -575,11 +674,37 @@ static int enqueue_macro(gbs_ctx* c, double H) {
     const int64_t l0 = c->launches;
     int rc;
     bool first = true;
+    const bool fused = fused_path(c);
     for (size_t q = 0; q < c->my_seq.size(); ++q) {
         const int k = c->my_seq[q];
         const int n = c->nk_all[k];
         const double h = H / (double)n;
         const bool last = (q + 1 == c->my_seq.size());
+        if (fused) {
+            // FE, then n/2 launches of two substeps: (LF1,LF2), ..., (LF_{n-1}, final)
+            const int L0 = 2;
+            if ((rc = step(c, 1, {Y, Y, L0, gbs::MODE_FE, h, 0.0, false}))) return rc;      // y1
+            int prev = Y, cur = L0;
+            for (int p = 0; p < n / 2; ++p) {
+                if (p + 1 < n / 2) {
+                    int outs[2], no = 0;
+                    for (int b = 2; b < 6 && no < 2; ++b)
+                        if (b != prev && b != cur) outs[no++] = b;
+                    if ((rc = pair_step(c, 3, {prev, cur, outs[0], outs[1], gbs::MODE_LF, 2.0 * h, 2.0 * h, 0.0,
+                                               false})))
+                        return rc;
+                    prev = outs[0];
+                    cur = outs[1];
+                } else {
+                    PairOperands fin{prev, cur, -1, ACC, first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, 2.0 * h, h,
+                                     0.5 * c->wk_all[k], last};
+                    fin.OA = ACC;     // unused by the FIN modes
+                    if ((rc = pair_step(c, 4, fin))) return rc;
+                }
+            }
+            first = false;
+            continue;
+        }
         if ((rc = step(c, 1, {Y, Y, B, gbs::MODE_FE, h, 0.0, false}))) return rc;            // y1
         if ((rc = step(c, 0, {B, Y, C, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;      // y2
         int prev = B, cur = C;
@@ -802,6 +927,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");
         if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback needs a single-GPU context");
@@ -938,7 +1064,7 @@ int gbs_query(const gbs_ctx* c, gbs_info* info) {
 }
 
 int gbs_kernel_time(gbs_ctx* c, int cls, double* total_ms, int64_t* launches, int reset) {
-    if (!c || cls < 0 || cls > 2) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
+    if (!c || cls < 0 || cls > 4) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
     int rc = harvest_timer(c);
     if (rc) return rc;
     if (total_ms) *total_ms = c->timer.total_ms[cls];

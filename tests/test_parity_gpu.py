@@ -135,6 +135,20 @@ def test_bulk_kernel_bitwise_equals_ldg_kernel(torch_cuda, n):
     assert np.array_equal(a[0], b[0])
 
 
+@pytest.mark.parametrize("cfg,n", [("c4", (128, 32, 24)), ("c4", (64, 16, 17)), ("c5", (64, 48, 40))])
+def test_two_substep_kernel_bitwise_equals_single_steps(torch_cuda, cfg, n):
+    """The temporally blocked kernel (two substeps per HBM pass) recomputes the
+    intermediate level with the same operations in the same order: bit-identical."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"fuse": 1})
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"fuse": 0})
+    assert np.array_equal(a[0], b[0])
+    S = sum(k + 1 for k in counts)
+    assert ib["kernel_launches"] == 2 * S
+    assert ia["kernel_launches"] == 2 * sum(1 + k // 2 for k in counts)
+
+
 @pytest.mark.parametrize("cfg,n,M,wset", CASES)
 def test_reduced_every_macro_step(torch_cuda, cfg, n, M, wset):
     w = reduced(cfg, n, macro_steps=M, weights=wset)
@@ -197,7 +211,7 @@ def test_graph_replay_is_bitwise_identical(torch_cuda):
 
 
 @pytest.mark.parametrize("cfg,n,slabs", [("c4", (40, 36, 32), 2), ("c4", (40, 36, 32), 4),
-                                         ("c4", (128, 32, 36), 3),
+                                         ("c4", (128, 32, 36), 3), ("c5", (64, 32, 32), 4),
                                          ("c5", (36, 20, 24), 3), ("c2", (96, 64, 1), 4),
                                          ("c3", (80, 48, 1), 3)])
 def test_loopback_slabs(torch_cuda, cfg, n, slabs):
