@@ -177,42 +177,33 @@ def run_reference(a):
 
 # ------------------------------------------------------------------------------ our arm
 def run_ours(a):
-    import numpy as np
     import torch
-    import torch.distributed as dist
 
     from gbs_inputs import make_ic
     from paper_1907_11771_b200 import gbs
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1907_11771_b200 import dist as pdist
+    rank, world, local = pdist.env()
     if world != a.gpus:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pdist.init("nccl", dev)
     w, counts, wd, H = workload_and_scheme(a.config)
     y0 = make_ic(w)                                   # host IC (same recipe as the oracle's)
     stream = torch.cuda.Stream()
     dist_desc = None
     if world > 1:
-        obj = [gbs.gbs_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
+        nccl_id = pdist.broadcast_bytes(gbs.gbs_nccl_unique_id() if rank == 0 else None, src=0)
         dist_desc = {"rank": rank, "world": world, "device": local, "groups": a.groups,
-                     "nccl_id": obj[0]}
+                     "nccl_id": nccl_id}
 
     def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+        pdist.barrier(sync_cuda=True)
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return pdist.max_over_ranks(x, dev)
 
     with torch.cuda.stream(stream):
         st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream)
@@ -315,7 +306,7 @@ def run_ours(a):
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        torch.distributed.destroy_process_group()
     return 0
 
 

@@ -110,6 +110,46 @@ typedef struct gbs_info {
 
 typedef struct gbs_ctx gbs_ctx;
 
+/* A rank's share of the multi-GPU plan (gbs_plan; same planner as gbs_create). */
+typedef struct gbs_plan_info {
+    int32_t groups, slabs;         /* g sequence groups x s slabs, g * s = world */
+    int32_t my_group, my_slab;     /* rank = my_group * slabs + my_slab */
+    int32_t my_sequences;          /* sequences of this rank's group */
+    int32_t my_n_k[32];            /* their step counts, ascending */
+    int64_t my_substeps;           /* sum (n_k + 1) over them */
+    int64_t critical_substeps;     /* max over groups of sum (n_k + 1) */
+    int64_t slab_z0, slab_nz;      /* this rank's planes of the slowest axis */
+} gbs_plan_info;
+
+/* Host-only planning (no device, no NCCL): the sequence-group x slab plan that
+ * gbs_create would use for (world, rank, groups) -- PAPER.md §3.6 (lines
+ * 388-400) balances sequences by RHS evaluations; groups are balanced by
+ * sum (n_k + 1) and the slowest axis is split into equal slabs.  Arguments as
+ * gbs_create (weights are not needed); groups = 0 lets the planner choose. */
+GBS_API int gbs_plan(const gbs_grid* grid, int stencil_order, int m, const int32_t* n_k, int world, int rank,
+                     int groups, gbs_plan_info* out);
+
+/* One point-to-point operation of the per-substep slab halo exchange. */
+typedef struct gbs_halo_op {
+    int32_t kind;       /* 0 = send, 1 = receive */
+    int32_t peer;       /* slab index of the partner (rank in the slab communicator) */
+    int32_t field;      /* state field (0 = u / p, 1 = v / u, 2 = v) */
+    int32_t pad;
+    int64_t plane0;     /* first local plane: interior planes are 0 .. nz_local-1, ghosts
+                           are -ghost .. -1 (low side) and nz_local .. nz_local+ghost-1 */
+    int64_t planes;     /* number of consecutive planes */
+} gbs_halo_op;
+
+/* Host-only: the ordered list of point-to-point operations one slab posts (inside
+ * one ncclGroupStart/End) to refresh the ghost planes of the fields in field_mask
+ * (bit f = field f) -- exactly the schedule gbs_advance uses.  For every pair of
+ * slabs the k-th send from a to b lands in the k-th receive at b from a (NCCL
+ * matches point-to-point operations in posting order), including slabs == 2,
+ * where both neighbours are the same peer.  Writes at most max_ops entries to
+ * ops and the number of operations to *n_ops. */
+GBS_API int gbs_halo_schedule(int slabs, int my_slab, int64_t nz_local, int ghost, uint32_t field_mask,
+                              gbs_halo_op* ops, int max_ops, int* n_ops);
+
 /* Create a context: validate, plan, allocate, and (multi-GPU) join NCCL.
  *   grid           problem description (copied)
  *   stencil_order  4 or 8 (centered FD, radius r = order / 2)

@@ -547,6 +547,30 @@ static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
 }
 
 // ---------------------------------------------------------------------------
+// The per-substep halo schedule of one slab (posted inside one NCCL group).
+// Per field: send up (my top interior planes -> the upper neighbour's low
+// ghosts), send down (my bottom interior planes -> the lower neighbour's high
+// ghosts), receive from below (into my low ghosts), receive from above (into
+// my high ghosts).  NCCL matches p2p operations per peer pair in posting order:
+// slab a's k-th send to b is b's k-th receive from a.  With 2 slabs both
+// neighbours are the same peer and the order send-up/send-down vs
+// recv-low/recv-high pairs a's top planes with b's low ghosts -- as required.
+// ---------------------------------------------------------------------------
+static std::vector<gbs_halo_op> halo_schedule(int slabs, int my_slab, int64_t nz, int G, unsigned mask) {
+    std::vector<gbs_halo_op> ops;
+    if (slabs < 2) return ops;
+    const int lo = (my_slab - 1 + slabs) % slabs, hi = (my_slab + 1) % slabs;
+    for (int f = 0; f < 32; ++f) {
+        if (!(mask & (1u << f))) continue;
+        ops.push_back({0, hi, f, 0, nz - G, G});      // send up
+        ops.push_back({0, lo, f, 0, 0, G});           // send down
+        ops.push_back({1, lo, f, 0, -G, G});          // receive from below
+        ops.push_back({1, hi, f, 0, nz, G});          // receive from above
+    }
+    return ops;
+}
+
+// ---------------------------------------------------------------------------
 // halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
 // whose stencil crosses the slab axis) -- ghost planes along the slowest axis
 // ---------------------------------------------------------------------------
@@ -585,16 +609,18 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0) {
     }
     if (nloc != 1) return fail(c, GBS_E_UNSUPPORTED, "loopback slabs with multi-GPU slabs");
     (void)S;
+    (void)cnt;
     auto& A = nccl::api();
-    const int lo = (c->my_slab - 1 + c->slabs) % c->slabs, hi = (c->my_slab + 1) % c->slabs;
     Slab& me = c->slab[0];
+    unsigned fm = 0;
+    for (int f : fields) fm |= 1u << f;
+    const std::vector<gbs_halo_op> ops = halo_schedule(c->slabs, c->my_slab, me.nz, (int)G, fm);
     NC(c, A.GroupStart());
-    for (int f : fields) {
-        double* mine = field_ptr(c, me, b, f);
-        NC(c, A.Send(mine, cnt, nccl::ncclFloat64, lo, c->comm_slab, c->stream));                  // my bottom -> lo's top ghosts
-        NC(c, A.Send(mine + (me.nz - G) * P, cnt, nccl::ncclFloat64, hi, c->comm_slab, c->stream)); // my top -> hi's bottom ghosts
-        NC(c, A.Recv(mine - G * P, cnt, nccl::ncclFloat64, lo, c->comm_slab, c->stream));
-        NC(c, A.Recv(mine + me.nz * P, cnt, nccl::ncclFloat64, hi, c->comm_slab, c->stream));
+    for (const auto& op : ops) {
+        double* p = field_ptr(c, me, b, op.field) + op.plane0 * P;
+        const size_t n = (size_t)(op.planes * P);
+        if (op.kind == 0) NC(c, A.Send(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, c->stream));
+        else NC(c, A.Recv(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, c->stream));
     }
     NC(c, A.GroupEnd());
     return GBS_OK;
@@ -795,12 +821,110 @@ void gbs_destroy(gbs_ctx* c) {
     delete c;
 }
 
-static int build_ctx(gbs_ctx* c) {
-    int rc;
-    // the sequences of this rank's group
-    auto grp = partition(c->nk_all, c->groups);
-    c->my_seq = grp[c->my_group];
-    if ((rc = alloc_state(c))) return rc;
+static int build_ctx(gbs_ctx* c) { return alloc_state(c); }
+
+// Validate the grid and the scheme (weights only when w_k != NULL) into c.
+static int validate(gbs_ctx* c, const gbs_grid* g, int stencil_order, int m, const int32_t* n_k,
+                    const double* w_k) {
+    c->pde = g->pde;
+    if (g->pde == GBS_ADV1D) { c->ndim = 1; c->F = 1; }
+    else if (g->pde == GBS_ACOUSTIC2D) { c->ndim = 2; c->F = 3; }
+    else if (g->pde == GBS_WAVE3D) { c->ndim = 3; c->F = 2; }
+    else return fail(c, GBS_E_INVAL, "grid.pde=%d is not a known PDE", g->pde);
+    if (g->ndim != c->ndim) return fail(c, GBS_E_INVAL, "grid.ndim=%d does not match the PDE", g->ndim);
+    if (stencil_order != 4 && stencil_order != 8)
+        return fail(c, GBS_E_INVAL, "stencil_order=%d (must be 4 or 8)", stencil_order);
+    c->order = stencil_order;
+    c->R = stencil_order / 2;
+    for (int d = 0; d < 3; ++d) {
+        c->n[d] = g->n[d];
+        c->len[d] = g->length[d] == 0.0 ? 1.0 : g->length[d];
+        if (d < c->ndim) {
+            if (g->n[d] < 2 * c->R + 1)
+                return fail(c, GBS_E_INVAL, "grid.n[%d]=%lld < 2r+1=%d", d, (long long)g->n[d], 2 * c->R + 1);
+            if (g->n[d] > (int64_t)1 << 30)
+                return fail(c, GBS_E_INVAL, "grid.n[%d]=%lld too large", d, (long long)g->n[d]);
+            if (!(c->len[d] > 0.0) || !std::isfinite(c->len[d]))
+                return fail(c, GBS_E_INVAL, "grid.length[%d] must be positive", d);
+        } else if (g->n[d] != 1) {
+            return fail(c, GBS_E_INVAL, "grid.n[%d] must be 1 for a %d-D PDE", d, c->ndim);
+        }
+    }
+    c->points = c->n[0] * c->n[1] * c->n[2];
+    c->nslow = c->n[c->ndim - 1];
+    c->plane = c->points / c->nslow;
+
+    if (m < 1 || m > 32) return fail(c, GBS_E_INVAL, "m=%d (must be 1..32)", m);
+    std::vector<std::pair<int, double>> seq;
+    for (int i = 0; i < m; ++i) {
+        if (n_k[i] < 2 || n_k[i] % 2) return fail(c, GBS_E_INVAL, "n_k[%d]=%d must be even and >= 2", i, n_k[i]);
+        if (n_k[i] > 1 << 20) return fail(c, GBS_E_INVAL, "n_k[%d]=%d too large", i, n_k[i]);
+        for (int j = 0; j < i; ++j)
+            if (n_k[j] == n_k[i]) return fail(c, GBS_E_INVAL, "n_k[%d]=n_k[%d]=%d duplicate", j, i, n_k[i]);
+        if (w_k && !std::isfinite(w_k[i])) return fail(c, GBS_E_WEIGHTS, "w_k[%d] is not finite", i);
+        seq.push_back({n_k[i], w_k ? w_k[i] : 0.0});
+    }
+    std::sort(seq.begin(), seq.end());
+    if (w_k) {
+        double sw = 0.0, sa = 0.0;
+        for (auto& p : seq) { sw += p.second; sa += std::fabs(p.second); }
+        if (!(std::fabs(sw - 1.0) <= 1e-12 * sa))
+            return fail(c, GBS_E_WEIGHTS, "sum of weights = %.17g (must be 1 within 1e-12 * sum|w|)", sw);
+    }
+    for (auto& p : seq) { c->nk_all.push_back(p.first); c->wk_all.push_back(p.second); }
+    return GBS_OK;
+}
+
+// Plan g groups x s slabs for (rank, world) into c (no device work).
+static int make_plan(gbs_ctx* c, int rank, int world, int groups) {
+    if (world < 1 || rank < 0 || rank >= world) return fail(c, GBS_E_INVAL, "rank=%d world=%d", rank, world);
+    if (groups < 0 || (groups > 0 && world % groups))
+        return fail(c, GBS_E_INVAL, "groups=%d must divide world=%d", groups, world);
+    c->rank = rank;
+    c->world = world;
+    plan(c, groups);
+    if (c->groups * c->slabs != c->world)
+        return fail(c, GBS_E_INVAL, "no valid plan: groups=%d does not fit world=%d (m=%d, slowest axis %lld)",
+                    groups, world, (int)c->nk_all.size(), (long long)c->nslow);
+    c->my_group = c->rank / c->slabs;
+    c->my_slab = c->rank % c->slabs;
+    c->my_seq = partition(c->nk_all, c->groups)[c->my_group];
+    return GBS_OK;
+}
+
+int gbs_halo_schedule(int slabs, int my_slab, int64_t nz_local, int ghost, uint32_t field_mask, gbs_halo_op* ops,
+                      int max_ops, int* n_ops) {
+    if (!n_ops || (max_ops > 0 && !ops)) return fail(nullptr, GBS_E_INVAL, "n_ops or ops is NULL");
+    if (slabs < 1 || my_slab < 0 || my_slab >= slabs || ghost < 0 || nz_local < ghost)
+        return fail(nullptr, GBS_E_INVAL, "slabs=%d my_slab=%d nz_local=%lld ghost=%d", slabs, my_slab,
+                    (long long)nz_local, ghost);
+    const std::vector<gbs_halo_op> v = halo_schedule(slabs, my_slab, nz_local, ghost, field_mask);
+    *n_ops = (int)v.size();
+    for (int i = 0; i < (int)v.size() && i < max_ops; ++i) ops[i] = v[i];
+    return (int)v.size() <= max_ops ? GBS_OK : fail(nullptr, GBS_E_INVAL, "max_ops=%d < %d", max_ops, (int)v.size());
+}
+
+int gbs_plan(const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, int world, int rank, int groups,
+             gbs_plan_info* out) {
+    if (!g || !n_k || !out) return fail(nullptr, GBS_E_INVAL, "grid, n_k or out is NULL");
+    gbs_ctx c;
+    int rc = validate(&c, g, stencil_order, m, n_k, nullptr);
+    if (!rc) rc = make_plan(&c, rank, world, groups);
+    if (rc) { g_err = c.err; return rc; }
+    memset(out, 0, sizeof(*out));
+    out->groups = c.groups;
+    out->slabs = c.slabs;
+    out->my_group = c.my_group;
+    out->my_slab = c.my_slab;
+    out->my_sequences = (int)c.my_seq.size();
+    for (size_t i = 0; i < c.my_seq.size(); ++i) {
+        out->my_n_k[i] = c.nk_all[c.my_seq[i]];
+        out->my_substeps += c.nk_all[c.my_seq[i]] + 1;
+    }
+    out->critical_substeps = crit_path(c.nk_all, c.groups);
+    const int64_t nzl = c.nslow / c.slabs;
+    out->slab_z0 = c.my_slab * nzl;
+    out->slab_nz = nzl;
     return GBS_OK;
 }
 
@@ -812,68 +936,15 @@ int gbs_create(const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, 
     gbs_ctx* c = new (std::nothrow) gbs_ctx();
     if (!c) return fail(nullptr, GBS_E_NOMEM, "host allocation failed");
     auto bail = [&](int code) { g_err = c->err; gbs_destroy(c); return code; };
-
-    // ---- validate the problem
-    c->pde = g->pde;
-    if (g->pde == GBS_ADV1D) { c->ndim = 1; c->F = 1; }
-    else if (g->pde == GBS_ACOUSTIC2D) { c->ndim = 2; c->F = 3; }
-    else if (g->pde == GBS_WAVE3D) { c->ndim = 3; c->F = 2; }
-    else return bail(fail(c, GBS_E_INVAL, "grid.pde=%d is not a known PDE", g->pde));
-    if (g->ndim != c->ndim) return bail(fail(c, GBS_E_INVAL, "grid.ndim=%d does not match the PDE", g->ndim));
-    if (stencil_order != 4 && stencil_order != 8)
-        return bail(fail(c, GBS_E_INVAL, "stencil_order=%d (must be 4 or 8)", stencil_order));
-    c->order = stencil_order;
-    c->R = stencil_order / 2;
-    for (int d = 0; d < 3; ++d) {
-        c->n[d] = g->n[d];
-        c->len[d] = g->length[d] == 0.0 ? 1.0 : g->length[d];
-        if (d < c->ndim) {
-            if (g->n[d] < 2 * c->R + 1)
-                return bail(fail(c, GBS_E_INVAL, "grid.n[%d]=%lld < 2r+1=%d", d, (long long)g->n[d], 2 * c->R + 1));
-            if (g->n[d] > (int64_t)1 << 30)
-                return bail(fail(c, GBS_E_INVAL, "grid.n[%d]=%lld too large", d, (long long)g->n[d]));
-            if (!(c->len[d] > 0.0) || !std::isfinite(c->len[d]))
-                return bail(fail(c, GBS_E_INVAL, "grid.length[%d] must be positive", d));
-        } else if (g->n[d] != 1) {
-            return bail(fail(c, GBS_E_INVAL, "grid.n[%d] must be 1 for a %d-D PDE", d, c->ndim));
-        }
-    }
-    c->points = c->n[0] * c->n[1] * c->n[2];
-    c->nslow = c->n[c->ndim - 1];
-    c->plane = c->points / c->nslow;
-
-    // ---- validate the scheme
-    if (m < 1 || m > 32) return bail(fail(c, GBS_E_INVAL, "m=%d (must be 1..32)", m));
-    std::vector<std::pair<int, double>> seq;
-    for (int i = 0; i < m; ++i) {
-        if (n_k[i] < 2 || n_k[i] % 2)
-            return bail(fail(c, GBS_E_INVAL, "n_k[%d]=%d must be even and >= 2", i, n_k[i]));
-        if (n_k[i] > 1 << 20) return bail(fail(c, GBS_E_INVAL, "n_k[%d]=%d too large", i, n_k[i]));
-        for (int j = 0; j < i; ++j)
-            if (n_k[j] == n_k[i]) return bail(fail(c, GBS_E_INVAL, "n_k[%d]=n_k[%d]=%d duplicate", j, i, n_k[i]));
-        if (!std::isfinite(w_k[i])) return bail(fail(c, GBS_E_WEIGHTS, "w_k[%d] is not finite", i));
-        seq.push_back({n_k[i], w_k[i]});
-    }
-    std::sort(seq.begin(), seq.end());
-    double sw = 0.0, sa = 0.0;
-    for (auto& p : seq) { sw += p.second; sa += std::fabs(p.second); }
-    if (!(std::fabs(sw - 1.0) <= 1e-12 * sa))
-        return bail(fail(c, GBS_E_WEIGHTS, "sum of weights = %.17g (must be 1 within 1e-12 * sum|w|)", sw));
-    for (auto& p : seq) { c->nk_all.push_back(p.first); c->wk_all.push_back(p.second); }
+    int rc0 = validate(c, g, stencil_order, m, n_k, w_k);
+    if (rc0) return bail(rc0);
 
     // ---- device / stream
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
         return bail(fail(c, GBS_E_CUDA, "no CUDA device available (this library has no CPU path)"));
-    if (dist) {
-        if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
-            return bail(fail(c, GBS_E_INVAL, "dist rank=%d world=%d", dist->rank, dist->world));
-        c->rank = dist->rank; c->world = dist->world; c->device = dist->device;
-        if (dist->groups < 0 || (dist->groups > 0 && dist->world % dist->groups))
-            return bail(fail(c, GBS_E_INVAL, "dist.groups=%d must divide world=%d", dist->groups, dist->world));
-    } else {
-        cudaGetDevice(&c->device);
-    }
+    if (dist) c->device = dist->device;
+    else cudaGetDevice(&c->device);
     if (c->device < 0 || c->device >= ndev)
         return bail(fail(c, GBS_E_INVAL, "device %d out of range (%d devices)", c->device, ndev));
     if (cudaSetDevice(c->device) != cudaSuccess)
@@ -886,12 +957,8 @@ int gbs_create(const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, 
     }
 
     // ---- plan + communicators
-    plan(c, dist ? dist->groups : 0);
-    if (c->groups * c->slabs != c->world)
-        return bail(fail(c, GBS_E_INVAL, "no valid plan: groups=%d does not fit world=%d (m=%d, slowest axis %lld)",
-                         dist ? dist->groups : 0, c->world, m, (long long)c->nslow));
-    c->my_group = c->rank / c->slabs;
-    c->my_slab = c->rank % c->slabs;
+    if ((rc0 = make_plan(c, dist ? dist->rank : 0, dist ? dist->world : 1, dist ? dist->groups : 0)))
+        return bail(rc0);
     if (c->world > 1) {
         auto& A = nccl::api();
         if (!A.ok) return bail(fail(c, GBS_E_NCCL, "libnccl.so.2 not found"));

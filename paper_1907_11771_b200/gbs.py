@@ -26,7 +26,8 @@ FIELDS = {"adv1d": 1, "acoustic2d": 3, "wave3d": 2}
 NDIM = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
 
 EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_sync",
-           "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_set_option",
+           "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
+           "gbs_set_option",
            "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
 
 
@@ -53,6 +54,24 @@ class gbs_info(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class gbs_plan_info(ctypes.Structure):
+    _fields_ = [("groups", ctypes.c_int32), ("slabs", ctypes.c_int32), ("my_group", ctypes.c_int32),
+                ("my_slab", ctypes.c_int32), ("my_sequences", ctypes.c_int32),
+                ("my_n_k", ctypes.c_int32 * 32), ("my_substeps", ctypes.c_int64),
+                ("critical_substeps", ctypes.c_int64), ("slab_z0", ctypes.c_int64),
+                ("slab_nz", ctypes.c_int64)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "my_n_k"}
+        d["my_n_k"] = list(self.my_n_k[: self.my_sequences])
+        return d
+
+
+class gbs_halo_op(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("peer", ctypes.c_int32), ("field", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("plane0", ctypes.c_int64), ("planes", ctypes.c_int64)]
 
 
 class GbsError(RuntimeError):
@@ -92,6 +111,11 @@ def load(build_if_missing: bool = False):
     L.gbs_destroy.restype = None
     L.gbs_nccl_unique_id.argtypes = [vp]
     L.gbs_query.argtypes = [vp, ctypes.POINTER(gbs_info)]
+    L.gbs_plan.argtypes = [ctypes.POINTER(gbs_grid), ctypes.c_int, ctypes.c_int,
+                           ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                           ctypes.POINTER(gbs_plan_info)]
+    L.gbs_halo_schedule.argtypes = [ctypes.c_int, ctypes.c_int, i64, ctypes.c_int, ctypes.c_uint32,
+                                    ctypes.POINTER(gbs_halo_op), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     L.gbs_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     L.gbs_kernel_time.argtypes = [vp, ctypes.c_int, dp, ctypes.POINTER(i64), ctypes.c_int]
     L.gbs_strerror.argtypes = [ctypes.c_int]
@@ -99,7 +123,7 @@ def load(build_if_missing: bool = False):
     L.gbs_last_error.argtypes = [vp]
     L.gbs_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:
-        if name not in ("gbs_destroy", "gbs_strerror", "gbs_last_error"):
+        if name not in ("gbs_destroy", "gbs_strerror", "gbs_last_error"):  # int status
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -133,16 +157,42 @@ def gbs_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def gbs_create(pde: str, n: Sequence[int], stencil_order: int, n_k: Sequence[int],
-               w_k: Sequence[float], dist: Optional[dict] = None, stream=None,
-               length: Sequence[float] = (1.0, 1.0, 1.0)):
-    L = load()
+def _grid(pde: str, n: Sequence[int], length: Sequence[float] = (1.0, 1.0, 1.0)) -> gbs_grid:
     g = gbs_grid()
     g.pde = PDE[pde]
     g.ndim = NDIM[pde]
     for d in range(3):
         g.n[d] = int(n[d]) if d < len(n) else 1
         g.length[d] = float(length[d])
+    return g
+
+
+def gbs_plan(pde: str, n: Sequence[int], stencil_order: int, n_k: Sequence[int], world: int,
+             rank: int, groups: int = 0) -> dict:
+    """Host-only plan of gbs_create for (world, rank, groups): no device needed."""
+    g = _grid(pde, n)
+    nk = (ctypes.c_int32 * len(n_k))(*[int(x) for x in n_k])
+    info = gbs_plan_info()
+    _check(load().gbs_plan(ctypes.byref(g), int(stencil_order), len(n_k), nk, int(world), int(rank),
+                           int(groups), ctypes.byref(info)))
+    return info.as_dict()
+
+
+def gbs_halo_schedule(slabs: int, my_slab: int, nz_local: int, ghost: int, field_mask: int):
+    """Host-only: the ordered p2p halo operations of one slab (list of dicts)."""
+    ops = (gbs_halo_op * 256)()
+    n = ctypes.c_int()
+    _check(load().gbs_halo_schedule(int(slabs), int(my_slab), int(nz_local), int(ghost), int(field_mask),
+                                    ops, 256, ctypes.byref(n)))
+    return [{"kind": "send" if o.kind == 0 else "recv", "peer": o.peer, "field": o.field,
+             "plane0": o.plane0, "planes": o.planes} for o in ops[: n.value]]
+
+
+def gbs_create(pde: str, n: Sequence[int], stencil_order: int, n_k: Sequence[int],
+               w_k: Sequence[float], dist: Optional[dict] = None, stream=None,
+               length: Sequence[float] = (1.0, 1.0, 1.0)):
+    L = load()
+    g = _grid(pde, n, length)
     nk = (ctypes.c_int32 * len(n_k))(*[int(x) for x in n_k])
     wk = (ctypes.c_double * len(w_k))(*[float(x) for x in w_k])
     dp = None

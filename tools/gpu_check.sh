@@ -1,5 +1,4 @@
 #!/bin/bash
 set -x
 python -m pytest tests -m "gpu and not slow" -x -q 2>&1 | tail -5
-for f in 1 0; do timeout 300 python tools/probe_perf.py --config c5 --fuse $f; done
-timeout 300 python tools/probe_perf.py --config c4
+python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline --config c4 2>&1 | tail -1
