@@ -195,12 +195,19 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *   "time_kernels" 1/0   record a CUDA event pair around every stencil launch
  *                        (on the context stream) for gbs_kernel_time (default 0)
  *   "loopback"     s     emulate s z-slabs on this GPU with device-to-device
- *                        halo copies through the multi-GPU code path (tests)  */
+ *                        halo copies through the multi-GPU code path (tests)
+ *   "bulk"         1/0   TMA-pipelined 3-D kernels on grids that are multiples of
+ *                        their 64 x 16 tile (default 1; 0 = register-prefetch kernels)
+ *   "fuse"         1/0   two substeps per HBM pass on TMA grids (default 0)
+ *   "persistent"   1/0   1-D grids up to 7000 points with m <= 16: every macro step of
+ *                        a gbs_advance in one thread-block-cluster launch (default 1)
+ *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)  */
 GBS_API int gbs_set_option(gbs_ctx* ctx, const char* key, int64_t value);
 
 /* Accumulated device time (ms) and launch count of the timed kernels of a class
- * since the last reset: cls 0 = interior LF, 1 = FE (+LF1), 2 = final (average +
- * weighted accumulate).  reset = 1 clears the counters after reading. */
+ * since the last reset: cls 0 = interior LF, 1 = FE, 2 = final (average + weighted
+ * accumulate), 3 = two LF substeps in one pass, 4 = LF + final in one pass, 5 = the
+ * whole-run cluster kernel.  reset = 1 clears the counters after reading. */
 GBS_API int gbs_kernel_time(gbs_ctx* ctx, int cls, double* total_ms, int64_t* launches, int reset);
 
 GBS_API const char* gbs_strerror(int code);

@@ -18,6 +18,7 @@
 #include "gbs_kernels.cuh"
 #include "gbs_wave3d_tma.cuh"
 #include "gbs_wave3d_pair.cuh"
+#include "gbs_adv1d_cluster.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -118,8 +119,8 @@ struct KernelTimer {
     std::vector<cudaEvent_t> ev;      // pairs
     std::vector<int> cls;
     size_t used = 0;
-    double total_ms[5] = {0, 0, 0, 0, 0};
-    int64_t launches[5] = {0, 0, 0, 0, 0};
+    double total_ms[6] = {0, 0, 0, 0, 0, 0};
+    int64_t launches[6] = {0, 0, 0, 0, 0, 0};
 };
 
 struct gbs_ctx {
@@ -152,6 +153,9 @@ struct gbs_ctx {
     bool use_graph = true;
     bool time_kernels = false;
     bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
+    bool use_persistent = true;       // one cluster launch per gbs_advance for small 1-D grids
+    int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
+    double* d_wh = nullptr;
     bool use_fuse = false;            // two-substep (temporally blocked) kernels where eligible
                                       // (bit-exact, but latency-bound: off by default)
     bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
@@ -759,6 +763,63 @@ static int enqueue_macro(gbs_ctx* c, double H) {
     return GBS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// small 1-D grids: the whole run in one cluster launch (K6)
+// ---------------------------------------------------------------------------
+static constexpr int kClusterMaxN = 7000;     // 4 nx doubles of shared memory per CTA
+
+static bool persistent_path(const gbs_ctx* c) {
+    const int m = (int)c->my_seq.size();
+    return c->use_persistent && c->pde == GBS_ADV1D && c->world == 1 && c->loopback == 1 && m >= 1 &&
+           m <= 16 && c->n[0] <= kClusterMaxN;
+}
+
+static int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H) {
+    const int m = (int)c->my_seq.size();
+    if (!c->d_nk) {
+        std::vector<int> nk;
+        std::vector<double> wh;
+        for (int k : c->my_seq) { nk.push_back(c->nk_all[k]); wh.push_back(0.5 * c->wk_all[k]); }
+        CU(c, cudaMalloc(&c->d_nk, sizeof(int) * m));
+        CU(c, cudaMalloc(&c->d_wh, sizeof(double) * m));
+        CU(c, cudaMemcpyAsync(c->d_nk, nk.data(), sizeof(int) * m, cudaMemcpyHostToDevice, c->stream));
+        CU(c, cudaMemcpyAsync(c->d_wh, wh.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+    }
+    gbs::Adv1DClusterArgs a;
+    a.Y = field_ptr(c, c->slab[0], c->yb, 0);
+    a.nx = (int)c->n[0];
+    a.sx = c->n[0] / c->len[0];
+    a.H = H;
+    a.macro_steps = macro_steps;
+    a.nk = c->d_nk;
+    a.wh = c->d_wh;
+    a.nonfinite = c->d_flag;
+    const size_t smem = sizeof(double) * 4 * (size_t)a.nx;
+    void (*kern)(const gbs::Adv1DClusterArgs) =
+        c->R == 2 ? gbs::adv1d_cluster_run<2> : gbs::adv1d_cluster_run<4>;
+    CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (m > 8) CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)m);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)m;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, 5, &end))) return rc;
+    CU(c, cudaLaunchKernelEx(&cfg, kern, a));
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    c->launches++;
+    return GBS_OK;
+}
+
 static int check_flag(gbs_ctx* c) {
     int h = 0;
     CU(c, cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -810,6 +871,8 @@ void gbs_destroy(gbs_ctx* c) {
     free_state(c);
     if (c->d_flag) cudaFree(c->d_flag);
     if (c->d_gather) cudaFree(c->d_gather);
+    if (c->d_nk) cudaFree(c->d_nk);
+    if (c->d_wh) cudaFree(c->d_wh);
     for (auto e : c->timer.ev) cudaEventDestroy(e);
     auto& A = nccl::api();
     if (A.ok) {
@@ -995,6 +1058,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "persistent") { c->use_persistent = value != 0; return GBS_OK; }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");
         if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback needs a single-GPU context");
@@ -1034,6 +1098,12 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
     if (!(H > 0.0) || !std::isfinite(H)) return fail(c, GBS_E_INVAL, "H=%g must be positive and finite", H);
     CU(c, cudaSetDevice(c->device));
     int rc;
+    if (macro_steps > 0 && persistent_path(c)) {
+        if ((rc = launch_cluster_run(c, macro_steps, H))) return rc;
+        c->macro_done += macro_steps;
+        c->t += H * (double)macro_steps;
+        return GBS_OK;
+    }
     const bool graph = c->use_graph && !c->time_kernels && macro_steps > 0;
     if (graph && c->graph_H != H) {
         for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
@@ -1131,7 +1201,7 @@ int gbs_query(const gbs_ctx* c, gbs_info* info) {
 }
 
 int gbs_kernel_time(gbs_ctx* c, int cls, double* total_ms, int64_t* launches, int reset) {
-    if (!c || cls < 0 || cls > 4) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
+    if (!c || cls < 0 || cls > 5) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
     int rc = harvest_timer(c);
     if (rc) return rc;
     if (total_ms) *total_ms = c->timer.total_ms[cls];

@@ -149,6 +149,24 @@ def test_two_substep_kernel_bitwise_equals_single_steps(torch_cuda, cfg, n):
     assert ia["kernel_launches"] == 2 * sum(1 + k // 2 for k in counts)
 
 
+@pytest.mark.parametrize("n,steps,wset,M", [((256, 1, 1), (2, 4, 6, 8), "square8", 200),
+                                            ((77, 1, 1), (2, 4, 6, 8), "square8", 30),
+                                            ((3000, 1, 1), tuple(range(2, 23, 2)), "GBS_8_6", 5)])
+def test_cluster_kernel_equals_per_substep_kernels(torch_cuda, n, steps, wset, M):
+    """K6: the whole run in one cluster launch (one CTA per sequence, DSMEM combine)
+    against the per-substep kernels (bit for bit) and the oracle."""
+    w = reduced("c1", n, macro_steps=M).with_(steps=steps, weights=wset)
+    counts, ws, _ = W.scheme(wset, steps)
+    wd = W.to_double(ws)
+    H = S.macro_step_H(w.pde, w.order, w.n, counts, wd)
+    y0, a, ia = run_gpu(torch_cuda, w, counts, wd, H, M, opts={"persistent": 1})
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, M, opts={"persistent": 0})
+    assert ia["kernel_launches"] == 1 and ib["kernel_launches"] == M * sum(k + 1 for k in counts)
+    assert np.array_equal(a[0], b[0])
+    o = run_oracle(w, y0, counts, wd, H, M)
+    assert_parity(a[0], o[0], what="cluster kernel")
+
+
 @pytest.mark.parametrize("cfg,n,M,wset", CASES)
 def test_reduced_every_macro_step(torch_cuda, cfg, n, M, wset):
     w = reduced(cfg, n, macro_steps=M, weights=wset)
