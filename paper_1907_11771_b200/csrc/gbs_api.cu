@@ -516,7 +516,8 @@ static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
     gbs::tma::PairArgs a;
     a.Au = field_ptr(c, s, op.OA, 0); a.Av = field_ptr(c, s, op.OA, 1);
     a.Bu = field_ptr(c, s, op.OB, 0); a.Bv = field_ptr(c, s, op.OB, 1);
-    a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1); a.Pu = field_ptr(c, s, op.P, 0);
+    a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1);
+    a.Pu = field_ptr(c, s, op.P, 0); a.Pv = field_ptr(c, s, op.P, 1);
     a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
     a.plane = c->plane;
     const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];

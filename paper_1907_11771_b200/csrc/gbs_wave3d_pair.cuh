@@ -10,22 +10,26 @@
 //     LF :  u_b = S_u + cfB v_a,                 v_b = S_v + cfB lap(u_a)
 //     FIN:  acc (+)= wh (S_u + u_a + cfB v_a),   acc (+)= wh (S_v + v_a + cfB lap(u_a))
 // Because u_a is pointwise in (P_u, S_v), lap(u_a) needs only the tiles of P_u
-// and S_v: each stencil value u_a(x') is recomputed as fma(cfA, S_v(x'), P_u(x')),
-// exactly the operation the single-step kernel performs at x', and every sum is
-// formed in the same order -- so the pair kernel is bit-identical to two
-// launches of wave3d_step(_tma) (tested), while moving 32 B read + 32 B write
-// per point for two substeps instead of 96 B (LF + LF).
+// and S_v: u_a(x') = fma(cfA, S_v(x'), P_u(x')) is exactly the operation the
+// single-step kernel performs at x', and every sum is formed in the same order,
+// so the pair kernel is bit-identical to two single-step launches (tested)
+// while moving 32 B read + 32 B write per point for two substeps instead of 96 B.
 //
 // Outputs go to buffers distinct from P and S (their halos are read by
 // neighbouring CTAs): LF writes y_{n+1} -> (Au, Av) and y_{n+2} -> (Bu, Bv);
 // FIN writes only the accumulator (Bu, Bv).
 //
-// Pipeline (per CTA: 64x16 tile, 16 consumer warps x 2 points + 1 producer
-// warp), stage for iteration i (plane z = z0 + i) carries:
-//   tiles of S_u, S_v, P_u at plane z (centre column with y-halo + x strips, as
-//   in gbs_wave3d_tma.cuh), the centre boxes of S_u, S_v, P_u at plane z + R
-//   (fronts of the two register queues, lap(S_u) and lap(u_a) along z), P_v at
-//   plane z, and the accumulator at plane z (FINACC).
+// Pipeline (64x16 tile, 16 warps x 2 points; lane 0 of warp 0 also issues TMA):
+//   stage i (D-deep ring): S_u tile of plane z = z0+i (x/y stencil of lap(S_u)),
+//     S_v and P_u tiles of plane z+R (to build the u_a tile of plane z+R), the
+//     S_u centre box of plane z+R (front of the S_u register queue)
+//   ua ring (R+2 deep): u_a tiles, the one of plane p built by all warps at
+//     iteration p-R and read (x/y stencil of lap(u_a)) at iteration p, so the
+//     builder never waits on the readers of the same plane; per-slot full/empty
+//     mbarriers (16 warp arrivals) with two iterations of slack
+//   own-point streams (S_v and P_v of plane z, the accumulator) by 128-bit loads
+//     issued one iteration ahead.
+// z neighbours of S_u and u_a live in two register queues of 2R+1 planes.
 #pragma once
 
 #include "gbs_wave3d_tma.cuh"
@@ -37,15 +41,20 @@ template <int R, int MODEB>
 struct PairLayout {
     static constexpr int SH = TY + 2 * R;
     static constexpr int NACC = (MODEB == MODE_FINACC) ? 2 : 0;
-    static constexpr int D = (MODEB == MODE_FINACC) ? 2 : 3;
+    static constexpr int D = 2;                            // TMA stages
+    static constexpr int RG = (MODEB == MODE_FINACC) ? R + 1 : R + 2;   // u_a ring
     static constexpr int CENTER = SH * TX;
     static constexpr int STRIP = TY * R;
     static constexpr int TILE = CENTER + 2 * STRIP;
     static constexpr int PWT = TY * TX;
-    // stage: 3 tiles | 3 fronts | P_v | acc (NACC)
-    static constexpr int STAGE = 3 * TILE + (4 + NACC) * PWT;
-    static constexpr size_t bytes = (size_t)D * STAGE * 8 + (2 * D) * 8;
+    // stage: S_u tile (z) | S_v tile (z+R) | P_u tile (z+R) | S_u centre (z+R) |
+    //        S_v centre (z) | P_v centre (z) | accumulator (z, FINACC)
+    static constexpr int STAGE = 3 * TILE + (3 + NACC) * PWT;
+    static constexpr size_t stage_doubles = (size_t)D * STAGE;
+    static constexpr size_t ring_doubles = (size_t)RG * TILE;
+    static constexpr size_t bytes = (stage_doubles + ring_doubles) * 8 + (2 * D + 2 * RG + 1) * 8;
     static constexpr uint32_t stage_bytes = STAGE * 8;
+    static constexpr uint32_t tile_bytes = TILE * 8;
 };
 
 struct PairMaps {
@@ -58,7 +67,7 @@ struct PairMaps {
 struct PairArgs {
     double* Au; double* Av;           // y_{n+1} (LF)
     double* Bu; double* Bv;           // y_{n+2} (LF) or the accumulator (FIN)
-    const double* Su; const double* Sv; const double* Pu;   // for the register-queue warm-up
+    const double* Su; const double* Sv; const double* Pu; const double* Pv;
     int nx, ny, nz, zchunk;
     int64_t plane;
     double sx2, sy2, sz2;
@@ -70,12 +79,17 @@ template <int R, int MODEB, bool SLAB>
 __global__ void __launch_bounds__(512, 1)
 wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int zbase) {
     using L = PairLayout<R, MODEB>;
-    constexpr int D = L::D, TILE = L::TILE, PWT = L::PWT, STAGE = L::STAGE;
+    constexpr int D = L::D, RG = L::RG, TILE = L::TILE, STAGE = L::STAGE;
     extern __shared__ __align__(128) double smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)D * STAGE);
+    double* stages = smem;
+    double* ring = smem + L::stage_doubles;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + L::ring_doubles);
     uint64_t* empty = full + D;
+    uint64_t* ua_full = empty + D;
+    uint64_t* ua_empty = ua_full + RG;
+    uint64_t* init = ua_empty + RG;
 
-    const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
+    const int tx = threadIdx.x, ty = threadIdx.y, lane = tx, t = ty * 32 + tx;
     const int nx = A.nx, ny = A.ny, nz = A.nz;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const int z0 = blockIdx.z * A.zchunk;
@@ -84,59 +98,77 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         if constexpr (SLAB) return z + zbase;
         else return wrap_once(z, nz);
     };
-
-    if (ty == 0 && lane == 0) {
-        for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TY); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    // Producer = lane 0 of warp 0 (a dedicated 17th warp would be allocated as 20
-    // warps and cap the consumers at 96 registers).  Stage i is issued at the top
-    // of iteration i - D + 1, after its slot's previous use (iteration i - D) has
-    // been released by all 16 warps.
-    const bool producer = (ty == 0 && lane == 0);
-    auto issue_stage = [&](int i) {
-        const CUtensorMap* maps[3][3] = {{&M.su_a, &M.su_b, &M.su_c}, {&M.sv_a, &M.sv_b, &M.sv_c},
-                                         {&M.pu_a, &M.pu_b, &M.pu_c}};
-        const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
-        const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
-        const int s = i % D;
-        if (i >= D) mbar_wait(&empty[s], (uint32_t)(((i / D) - 1) & 1));
-        mbar_expect_tx(&full[s], L::stage_bytes);
-        double* st = smem + (size_t)s * STAGE;
-        const int z = zc(z0 + i), zf = zc(z0 + i + R);
-#pragma unroll
-        for (int f = 0; f < 3; ++f) {
-            double* t = st + f * TILE;
-            tma_load_3d(t, maps[f][1], x0, ytop, z, &full[s]);
-            tma_load_3d(t + R * TX, maps[f][0], x0, y0, z, &full[s]);
-            tma_load_3d(t + (R + TY) * TX, maps[f][1], x0, ybot, z, &full[s]);
-            tma_load_3d(t + L::CENTER, maps[f][2], xl, y0, z, &full[s]);
-            tma_load_3d(t + L::CENTER + L::STRIP, maps[f][2], xr, y0, z, &full[s]);
-            tma_load_3d(st + 3 * TILE + f * PWT, maps[f][0], x0, y0, zf, &full[s]);   // front
-        }
-        tma_load_3d(st + 3 * TILE + 3 * PWT, &M.pv, x0, y0, z, &full[s]);
-        if constexpr (MODEB == MODE_FINACC) {
-            tma_load_3d(st + 3 * TILE + 4 * PWT, &M.acc_u, x0, y0, z, &full[s]);
-            tma_load_3d(st + 3 * TILE + 5 * PWT, &M.acc_v, x0, y0, z, &full[s]);
-        }
-    };
-    if (producer) {
-        prefetch_map(&M.su_a); prefetch_map(&M.su_b); prefetch_map(&M.su_c);
-        prefetch_map(&M.sv_a); prefetch_map(&M.sv_b); prefetch_map(&M.sv_c);
-        prefetch_map(&M.pu_a); prefetch_map(&M.pu_b); prefetch_map(&M.pu_c); prefetch_map(&M.pv);
-        if constexpr (MODEB == MODE_FINACC) { prefetch_map(&M.acc_u); prefetch_map(&M.acc_v); }
-        for (int i = 0; i < D - 1 && i < niter; ++i) issue_stage(i);
-    }
-
-    // ===================== all 16 warps compute =====================
     const int64_t plane = A.plane;
     const int64_t own = (int64_t)(y0 + ty) * nx + x0 + 2 * tx;
     auto zoff = [&](int z) -> int64_t {
         if constexpr (SLAB) return (int64_t)z * plane;
         else return (int64_t)wrap_once(z, nz) * plane;
     };
+    const bool producer = (ty == 0 && lane == 0);
+    const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
+    const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
+
+    auto load_tile = [&](double* dst, const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int z,
+                         uint64_t* bar) {
+        tma_load_3d(dst, b, x0, ytop, z, bar);
+        tma_load_3d(dst + R * TX, a, x0, y0, z, bar);
+        tma_load_3d(dst + (R + TY) * TX, b, x0, ybot, z, bar);
+        tma_load_3d(dst + L::CENTER, c, xl, y0, z, bar);
+        tma_load_3d(dst + L::CENTER + L::STRIP, c, xr, y0, z, bar);
+    };
+    auto issue_stage = [&](int i) {
+        const int s = i % D;
+        if (i >= D) mbar_wait(&empty[s], (uint32_t)(((i / D) - 1) & 1));
+        mbar_expect_tx(&full[s], L::stage_bytes);
+        double* st = stages + (size_t)s * STAGE;
+        const int z = zc(z0 + i), zf = zc(z0 + i + R);
+        load_tile(st, &M.su_a, &M.su_b, &M.su_c, z, &full[s]);
+        load_tile(st + TILE, &M.sv_a, &M.sv_b, &M.sv_c, zf, &full[s]);
+        load_tile(st + 2 * TILE, &M.pu_a, &M.pu_b, &M.pu_c, zf, &full[s]);
+        tma_load_3d(st + 3 * TILE, &M.su_a, x0, y0, zf, &full[s]);
+        tma_load_3d(st + 3 * TILE + L::PWT, &M.sv_a, x0, y0, z, &full[s]);
+        tma_load_3d(st + 3 * TILE + 2 * L::PWT, &M.pv, x0, y0, z, &full[s]);
+        if constexpr (MODEB == MODE_FINACC) {
+            tma_load_3d(st + 3 * TILE + 3 * L::PWT, &M.acc_u, x0, y0, z, &full[s]);
+            tma_load_3d(st + 3 * TILE + 4 * L::PWT, &M.acc_v, x0, y0, z, &full[s]);
+        }
+    };
+    // u_a tile of relative plane p from S_v / P_u tiles at sv / pu into its ring slot
+    auto build = [&](const double* sv, const double* pu, int p) {
+        const int slot = p % RG, use = p / RG;
+        if (use >= 1) mbar_wait(&ua_empty[slot], (uint32_t)((use - 1) & 1));
+        const double2* v2 = reinterpret_cast<const double2*>(sv);
+        const double2* p2 = reinterpret_cast<const double2*>(pu);
+        double2* o2 = reinterpret_cast<double2*>(ring + (size_t)slot * TILE);
+        for (int e = t; e < TILE / 2; e += 32 * TY) {
+            const double2 a = v2[e], b = p2[e];
+            o2[e] = make_double2(fma(A.cfA, a.x, b.x), fma(A.cfA, a.y, b.y));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ua_full[slot]);
+    };
+
+    if (producer) {
+        for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TY); }
+        for (int s = 0; s < RG; ++s) { mbar_init(&ua_full[s], TY); mbar_init(&ua_empty[s], TY); }
+        mbar_init(init, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // ---- prologue: u_a tiles of planes z0 .. z0+R-1 (S_v, P_u tiles staged in the stage area)
+    static_assert(2 * R * TILE <= (int)L::stage_doubles, "prologue tiles must fit the stage area");
+    if (producer) {
+        prefetch_map(&M.su_a); prefetch_map(&M.su_b); prefetch_map(&M.su_c);
+        prefetch_map(&M.sv_a); prefetch_map(&M.sv_b); prefetch_map(&M.sv_c);
+        prefetch_map(&M.pu_a); prefetch_map(&M.pu_b); prefetch_map(&M.pu_c); prefetch_map(&M.pv);
+        if constexpr (MODEB == MODE_FINACC) { prefetch_map(&M.acc_u); prefetch_map(&M.acc_v); }
+        mbar_expect_tx(init, 2 * R * L::tile_bytes);
+        for (int p = 0; p < R; ++p) {
+            load_tile(stages + (size_t)(2 * p) * TILE, &M.sv_a, &M.sv_b, &M.sv_c, zc(z0 + p), init);
+            load_tile(stages + (size_t)(2 * p + 1) * TILE, &M.pu_a, &M.pu_b, &M.pu_c, zc(z0 + p), init);
+        }
+    }
     using V = Vec<2>;
     V qs[2 * R + 1], qa[2 * R + 1];          // S_u and u_a at z-R .. z+R (own points)
 #pragma unroll
@@ -147,96 +179,97 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
 #pragma unroll
         for (int v = 0; v < 2; ++v) qa[j].v[v] = fma(A.cfA, sv.v[v], pu.v[v]);
     }
+    mbar_wait(init, 0);
+    for (int p = 0; p < R && p < niter; ++p)
+        build(stages + (size_t)(2 * p) * TILE, stages + (size_t)(2 * p + 1) * TILE, p);
+    __syncthreads();                          // the stage area is free again
+    if (producer)
+        for (int i = 0; i < D - 1 && i < niter; ++i) issue_stage(i);
+
+    const int crow = (R + ty) * TX + 2 * tx;
+    auto window_off = [&](int k) {
+        const int col = 2 * tx - R + 2 * k;
+        return col < 0 ? L::CENTER + ty * R + (col + R)
+             : col >= TX ? L::CENTER + L::STRIP + ty * R + (col - TX)
+                         : (R + ty) * TX + col;
+    };
+    // lap at the thread's two points from a tile (x, y) and a register queue (z)
+    auto laplacian = [&](const double* tile, const V* q, double* lap, double* centre) {
+        double xw[2 * R + 2];
+#pragma unroll
+        for (int k = 0; k <= R; ++k) {
+            const double2 a = *reinterpret_cast<const double2*>(tile + window_off(k));
+            xw[2 * k] = a.x; xw[2 * k + 1] = a.y;
+        }
+        double lx[2], ly[2], lz[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            centre[v] = xw[R + v];
+            lx[v] = FD<R>::b0() * xw[R + v]; ly[v] = lx[v]; lz[v] = lx[v];
+        }
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            const double2 up = *reinterpret_cast<const double2*>(tile + crow - j * TX);
+            const double2 dn = *reinterpret_cast<const double2*>(tile + crow + j * TX);
+            const double upv[2] = {up.x, up.y}, dnv[2] = {dn.x, dn.y};
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                lx[v] = fma(FD<R>::b(j), xw[R + v + j] + xw[R + v - j], lx[v]);
+                ly[v] = fma(FD<R>::b(j), dnv[v] + upv[v], ly[v]);
+                lz[v] = fma(FD<R>::b(j), q[R + j].v[v] + q[R - j].v[v], lz[v]);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < 2; ++v) lap[v] = fma(A.sx2, lx[v], fma(A.sy2, ly[v], A.sz2 * lz[v]));
+    };
 
     bool bad = false;
     for (int i = 0; i < niter; ++i) {
         const int s = i % D;
         if (producer && i + D - 1 < niter) issue_stage(i + D - 1);
         mbar_wait(&full[s], (uint32_t)((i / D) & 1));
-        double* st = smem + (size_t)s * STAGE;
-        const double* tS = st;                  // S_u tile
-        const double* tV = st + TILE;           // S_v tile
-        double* tP = st + 2 * TILE;             // P_u tile, turned into the u_a tile below
-        const double* fr = st + 3 * TILE + ty * TX + 2 * tx;   // fronts + pointwise, own column
+        const double* st = stages + (size_t)s * STAGE;
+        V csv, cpv, cau, cav;                                    // own points of plane z
         {
-            const double2 fs = *reinterpret_cast<const double2*>(fr);
-            const double2 fv = *reinterpret_cast<const double2*>(fr + PWT);
-            const double2 fp = *reinterpret_cast<const double2*>(fr + 2 * PWT);
+            const double* pw = st + 3 * TILE + ty * TX + 2 * tx;
+            const double2 a = *reinterpret_cast<const double2*>(pw + L::PWT);
+            const double2 b = *reinterpret_cast<const double2*>(pw + 2 * L::PWT);
+            csv.v[0] = a.x; csv.v[1] = a.y; cpv.v[0] = b.x; cpv.v[1] = b.y;
+            cau.v[0] = cau.v[1] = cav.v[0] = cav.v[1] = 0.0;
+            if constexpr (MODEB == MODE_FINACC) {
+                const double2 c = *reinterpret_cast<const double2*>(pw + 3 * L::PWT);
+                const double2 d = *reinterpret_cast<const double2*>(pw + 4 * L::PWT);
+                cau.v[0] = c.x; cau.v[1] = c.y; cav.v[0] = d.x; cav.v[1] = d.y;
+            }
+        }
+        // the u_a tile of plane z+R, consumed R iterations from now
+        if (i + R < niter) build(st + TILE, st + 2 * TILE, i + R);
+        {   // queue fronts (plane z+R, own points)
+            const double2 fs = *reinterpret_cast<const double2*>(st + 3 * TILE + ty * TX + 2 * tx);
+            const double2 fv = *reinterpret_cast<const double2*>(st + TILE + crow);
+            const double2 fp = *reinterpret_cast<const double2*>(st + 2 * TILE + crow);
             qs[2 * R].v[0] = fs.x; qs[2 * R].v[1] = fs.y;
             qa[2 * R].v[0] = fma(A.cfA, fv.x, fp.x);
             qa[2 * R].v[1] = fma(A.cfA, fv.y, fp.y);
         }
-        // u_a = fma(cfA, S_v, P_u) over the whole tile (halo included), once, in place
-        {
-            const double2* v2 = reinterpret_cast<const double2*>(tV);
-            double2* p2 = reinterpret_cast<double2*>(tP);
-            for (int e = ty * 32 + tx; e < TILE / 2; e += 32 * TY) {
-                const double2 a = v2[e], b = p2[e];
-                p2[e] = make_double2(fma(A.cfA, a.x, b.x), fma(A.cfA, a.y, b.y));
-            }
-        }
-        __syncthreads();
-        // x windows (columns 2tx - R .. 2tx + R + 1) of S_u and u_a
-        double xs[2 * R + 2], xa[2 * R + 2];
-#pragma unroll
-        for (int k = 0; k <= R; ++k) {
-            const int col = 2 * tx - R + 2 * k;
-            const int off = col < 0 ? L::CENTER + ty * R + (col + R)
-                          : col >= TX ? L::CENTER + L::STRIP + ty * R + (col - TX)
-                                      : (R + ty) * TX + col;
-            const double2 a = *reinterpret_cast<const double2*>(tS + off);
-            const double2 c = *reinterpret_cast<const double2*>(tP + off);
-            xs[2 * k] = a.x; xs[2 * k + 1] = a.y;
-            xa[2 * k] = c.x; xa[2 * k + 1] = c.y;
-        }
-        const int crow = (R + ty) * TX + 2 * tx;
-        double lsx[2], lsy[2], lsz[2], lax[2], lay[2], laz[2];
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            const double cs = xs[R + v], ca = xa[R + v];
-            lsx[v] = FD<R>::b0() * cs; lsy[v] = FD<R>::b0() * cs; lsz[v] = FD<R>::b0() * cs;
-            lax[v] = FD<R>::b0() * ca; lay[v] = FD<R>::b0() * ca; laz[v] = FD<R>::b0() * ca;
-        }
-#pragma unroll
-        for (int j = 1; j <= R; ++j) {
-            const double2 su = *reinterpret_cast<const double2*>(tS + crow - j * TX);
-            const double2 sd = *reinterpret_cast<const double2*>(tS + crow + j * TX);
-            const double2 au = *reinterpret_cast<const double2*>(tP + crow - j * TX);
-            const double2 ad = *reinterpret_cast<const double2*>(tP + crow + j * TX);
-            const double su2[2] = {su.x, su.y}, sd2[2] = {sd.x, sd.y};
-            const double au2[2] = {au.x, au.y}, ad2[2] = {ad.x, ad.y};
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-                lsx[v] = fma(FD<R>::b(j), xs[R + v + j] + xs[R + v - j], lsx[v]);
-                lsy[v] = fma(FD<R>::b(j), sd2[v] + su2[v], lsy[v]);
-                lsz[v] = fma(FD<R>::b(j), qs[R + j].v[v] + qs[R - j].v[v], lsz[v]);
-                lax[v] = fma(FD<R>::b(j), xa[R + v + j] + xa[R + v - j], lax[v]);
-                lay[v] = fma(FD<R>::b(j), ad2[v] + au2[v], lay[v]);
-                laz[v] = fma(FD<R>::b(j), qa[R + j].v[v] + qa[R - j].v[v], laz[v]);
-            }
-        }
-        const double* pvp = st + 3 * TILE + 3 * PWT + ty * TX + 2 * tx;
-        const double2 pv = *reinterpret_cast<const double2*>(pvp);
-        double2 accu = make_double2(0, 0), accv = make_double2(0, 0);
-        if constexpr (MODEB == MODE_FINACC) {
-            accu = *reinterpret_cast<const double2*>(pvp + PWT);
-            accv = *reinterpret_cast<const double2*>(pvp + 2 * PWT);
-        }
-        // centre values of S_v for step B (from the S_v tile)
-        const double2 svc = *reinterpret_cast<const double2*>(tV + crow);
+        double lapS[2], lapA[2], xs_c[2], xa_c[2];
+        laplacian(st, qs, lapS, xs_c);                          // S_u tile, plane z
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        const double pvv[2] = {pv.x, pv.y}, svv[2] = {svc.x, svc.y};
-        const double acu[2] = {accu.x, accu.y}, acv[2] = {accv.x, accv.y};
+        if (lane == 0) mbar_arrive(&empty[s]);                  // stage s consumed by this warp
+        {
+            const int slot = i % RG;
+            mbar_wait(&ua_full[slot], (uint32_t)((i / RG) & 1));
+            laplacian(ring + (size_t)slot * TILE, qa, lapA, xa_c);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ua_empty[slot]);
+        }
         double ua[2], va[2], ub[2], vb[2];
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-            const double lapS = fma(A.sx2, lsx[v], fma(A.sy2, lsy[v], A.sz2 * lsz[v]));
-            const double lapA = fma(A.sx2, lax[v], fma(A.sy2, lay[v], A.sz2 * laz[v]));
-            ua[v] = xa[R + v];                                   // = fma(cfA, S_v, P_u): step A, u
-            va[v] = combine<MODE_LF>(pvv[v], svv[v], lapS, 0.0, A.cfA, 0.0);      // step A, v
-            ub[v] = combine<MODEB>(xs[R + v], ua[v], va[v], acu[v], A.cfB, A.wh);  // step B, u
-            vb[v] = combine<MODEB>(svv[v], va[v], lapA, acv[v], A.cfB, A.wh);      // step B, v
+            ua[v] = xa_c[v];                                                      // step A, u
+            va[v] = combine<MODE_LF>(cpv.v[v], csv.v[v], lapS[v], 0.0, A.cfA, 0.0);   // step A, v
+            ub[v] = combine<MODEB>(xs_c[v], ua[v], va[v], cau.v[v], A.cfB, A.wh);     // step B, u
+            vb[v] = combine<MODEB>(csv.v[v], va[v], lapA[v], cav.v[v], A.cfB, A.wh);  // step B, v
             if constexpr (MODEB != MODE_LF) bad |= !isfinite(ub[v]) || !isfinite(vb[v]);
         }
         const int64_t o = zoff(z0 + i) + own;

@@ -1,3 +1,2 @@
 #!/bin/bash
-set -x
-python -m pytest tests -m "gpu and not slow" -x -q 2>&1 | tail -15
+python -m pytest tests -m "gpu and slow" -x -q --durations=10 2>&1 | tail -20
