@@ -312,22 +312,50 @@ def _sample_boxes(w, y0, counts, wd, H, centres):
 
 
 @pytest.mark.slow
-def test_c2_full_size(torch_cuda):
-    w = get_config("c2")
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_2d_full_size_whole_run(torch_cuda, cfg):
+    """The whole BASELINE.json run (C2: 1024^2, 50 macro steps; C3: 4096^2, 20) against the
+    oracle, checked every 10 macro steps over the full state."""
+    w = get_config(cfg)
     counts, wd, H = scheme_for(w)
-    M = 10
-    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, M)
-    o = run_oracle(w, y0, counts, wd, H, M)
-    assert_parity(g[0], o[0], what="c2 full, 10 macro steps")
+    gbs = gbs_mod()
+    torch = torch_cuda
+    y0 = make_ic(w)
+    ref = y0
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch.from_numpy(y0).cuda())
+        done = 0
+        while done < w.macro_steps:
+            k = min(10, w.macro_steps - done)
+            st.advance(k, H)
+            out = torch.empty(y0.shape, dtype=torch.float64, device="cuda")
+            st.read(out)
+            ref = C.advance(w.pde, w.order, ref, counts, wd, H, k)
+            done += k
+            assert_parity(out.cpu().numpy(), ref, what=f"{cfg} full, macro step {done}")
 
 
 @pytest.mark.slow
-def test_c3_full_size(torch_cuda):
-    w = get_config("c3")
+def test_c5_whole_run_conserves_means(torch_cuda):
+    """Property at full size: the whole C5 run (1024^3, 4 macro steps). The zero Fourier mode
+    of the 3-D wave evolves as u0' = v0, v0' = 0 with R(0)=1, R'(0)=sum w = 1, so the means of
+    u and v after M macro steps are mean(u) + M H mean(v) and mean(v) (to rounding)."""
+    torch = torch_cuda
+    gbs = gbs_mod()
+    w = get_config("c5")
     counts, wd, H = scheme_for(w)
-    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, 1)
-    o = run_oracle(w, y0, counts, wd, H, 1)
-    assert_parity(g[0], o[0], what="c3 full, 1 macro step")
+    y0 = make_ic(w)
+    mu0, mv0 = float(y0[0].mean()), float(y0[1].mean())
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch.from_numpy(y0).cuda())
+        st.advance(w.macro_steps, H)
+        out = torch.empty(y0.shape, dtype=torch.float64, device="cuda")
+        st.read(out)
+        mu, mv = float(out[0].mean()), float(out[1].mean())
+        rms = float(out[0].pow(2).mean().sqrt())
+        assert torch.isfinite(out).all()
+    assert abs(mu - (mu0 + w.macro_steps * H * mv0)) < 1e-12 and abs(mv - mv0) < 1e-12
+    assert 0.1 < rms < 10.0
 
 
 @pytest.mark.slow
