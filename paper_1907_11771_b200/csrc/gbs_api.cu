@@ -156,8 +156,8 @@ struct gbs_ctx {
     bool use_persistent = true;       // one cluster launch per gbs_advance for small 1-D grids
     int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
     double* d_wh = nullptr;
-    bool use_fuse = false;            // two-substep (temporally blocked) kernels where eligible
-                                      // (bit-exact, but latency-bound: off by default)
+    bool use_fuse = true;             // two-substep (temporally blocked) kernels where eligible
+                                      // (bit-exact)
     bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
     int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
@@ -378,7 +378,7 @@ static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY), L::bytes, st>>>(m, a, zbase);
+    gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY / 2), L::bytes, st>>>(m, a, zbase);
     return cudaSuccess;
 }
 template <int R, int MODE, bool SLAB>

@@ -76,10 +76,12 @@ struct PairArgs {
 };
 
 template <int R, int MODEB, bool SLAB>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(256, 1)
 wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int zbase) {
     using L = PairLayout<R, MODEB>;
-    constexpr int D = L::D, RG = L::RG, TILE = L::TILE, STAGE = L::STAGE;
+    constexpr int D = L::D, RG = L::RG, TILE = L::TILE, STAGE = L::STAGE, PWT = L::PWT;
+    constexpr int NW = TY / 2;                 // 8 warps; each thread owns 2 x 2 points
+    constexpr int Q = 2 * R + 1;
     extern __shared__ __align__(128) double smem[];
     double* stages = smem;
     double* ring = smem + L::stage_doubles;
@@ -99,7 +101,8 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         else return wrap_once(z, nz);
     };
     const int64_t plane = A.plane;
-    const int64_t own = (int64_t)(y0 + ty) * nx + x0 + 2 * tx;
+    const int r0 = 2 * ty;                     // the thread's rows r0, r0 + 1 of the tile
+    const int64_t own = (int64_t)(y0 + r0) * nx + x0 + 2 * tx;
     auto zoff = [&](int z) -> int64_t {
         if constexpr (SLAB) return (int64_t)z * plane;
         else return (int64_t)wrap_once(z, nz) * plane;
@@ -126,21 +129,21 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         load_tile(st + TILE, &M.sv_a, &M.sv_b, &M.sv_c, zf, &full[s]);
         load_tile(st + 2 * TILE, &M.pu_a, &M.pu_b, &M.pu_c, zf, &full[s]);
         tma_load_3d(st + 3 * TILE, &M.su_a, x0, y0, zf, &full[s]);
-        tma_load_3d(st + 3 * TILE + L::PWT, &M.sv_a, x0, y0, z, &full[s]);
-        tma_load_3d(st + 3 * TILE + 2 * L::PWT, &M.pv, x0, y0, z, &full[s]);
+        tma_load_3d(st + 3 * TILE + PWT, &M.sv_a, x0, y0, z, &full[s]);
+        tma_load_3d(st + 3 * TILE + 2 * PWT, &M.pv, x0, y0, z, &full[s]);
         if constexpr (MODEB == MODE_FINACC) {
-            tma_load_3d(st + 3 * TILE + 3 * L::PWT, &M.acc_u, x0, y0, z, &full[s]);
-            tma_load_3d(st + 3 * TILE + 4 * L::PWT, &M.acc_v, x0, y0, z, &full[s]);
+            tma_load_3d(st + 3 * TILE + 3 * PWT, &M.acc_u, x0, y0, z, &full[s]);
+            tma_load_3d(st + 3 * TILE + 4 * PWT, &M.acc_v, x0, y0, z, &full[s]);
         }
     };
-    // u_a tile of relative plane p from S_v / P_u tiles at sv / pu into its ring slot
+    // u_a tile of relative plane p from S_v / P_u tiles into its ring slot
     auto build = [&](const double* sv, const double* pu, int p) {
         const int slot = p % RG, use = p / RG;
         if (use >= 1) mbar_wait(&ua_empty[slot], (uint32_t)((use - 1) & 1));
         const double2* v2 = reinterpret_cast<const double2*>(sv);
         const double2* p2 = reinterpret_cast<const double2*>(pu);
         double2* o2 = reinterpret_cast<double2*>(ring + (size_t)slot * TILE);
-        for (int e = t; e < TILE / 2; e += 32 * TY) {
+        for (int e = t; e < TILE / 2; e += 32 * NW) {
             const double2 a = v2[e], b = p2[e];
             o2[e] = make_double2(fma(A.cfA, a.x, b.x), fma(A.cfA, a.y, b.y));
         }
@@ -149,8 +152,8 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     };
 
     if (producer) {
-        for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TY); }
-        for (int s = 0; s < RG; ++s) { mbar_init(&ua_full[s], TY); mbar_init(&ua_empty[s], TY); }
+        for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
+        for (int s = 0; s < RG; ++s) { mbar_init(&ua_full[s], NW); mbar_init(&ua_empty[s], NW); }
         mbar_init(init, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -169,15 +172,20 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
             load_tile(stages + (size_t)(2 * p + 1) * TILE, &M.pu_a, &M.pu_b, &M.pu_c, zc(z0 + p), init);
         }
     }
-    using V = Vec<2>;
-    V qs[2 * R + 1], qa[2 * R + 1];          // S_u and u_a at z-R .. z+R (own points)
+    // register queues of S_u and u_a at planes z-R .. z+R; point index 2*row + col
+    double qs[Q][4], qa[Q][4];
 #pragma unroll
     for (int j = 0; j < 2 * R; ++j) {
-        const int64_t o = zoff(z0 - R + j) + own;
-        qs[j] = V::ld(A.Su + o);
-        const V sv = V::ld(A.Sv + o), pu = V::ld(A.Pu + o);
+        const int64_t oz = zoff(z0 - R + j);
 #pragma unroll
-        for (int v = 0; v < 2; ++v) qa[j].v[v] = fma(A.cfA, sv.v[v], pu.v[v]);
+        for (int r = 0; r < 2; ++r) {
+            const int64_t o = oz + own + (int64_t)r * nx;
+            const double2 su = __ldg(reinterpret_cast<const double2*>(A.Su + o));
+            const double2 sv = __ldg(reinterpret_cast<const double2*>(A.Sv + o));
+            const double2 pu = __ldg(reinterpret_cast<const double2*>(A.Pu + o));
+            qs[j][2 * r] = su.x; qs[j][2 * r + 1] = su.y;
+            qa[j][2 * r] = fma(A.cfA, sv.x, pu.x); qa[j][2 * r + 1] = fma(A.cfA, sv.y, pu.y);
+        }
     }
     mbar_wait(init, 0);
     for (int p = 0; p < R && p < niter; ++p)
@@ -186,41 +194,64 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     if (producer)
         for (int i = 0; i < D - 1 && i < niter; ++i) issue_stage(i);
 
-    const int crow = (R + ty) * TX + 2 * tx;
-    auto window_off = [&](int k) {
-        const int col = 2 * tx - R + 2 * k;
-        return col < 0 ? L::CENTER + ty * R + (col + R)
-             : col >= TX ? L::CENTER + L::STRIP + ty * R + (col - TX)
-                         : (R + ty) * TX + col;
-    };
-    // lap at the thread's two points from a tile (x, y) and a register queue (z)
-    auto laplacian = [&](const double* tile, const V* q, double* lap, double* centre) {
-        double xw[2 * R + 2];
+    // x-window sources of the thread's two rows: columns 2tx - R + 2k
+    int woff[2][R + 1];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int k = 0; k <= R; ++k) {
-            const double2 a = *reinterpret_cast<const double2*>(tile + window_off(k));
-            xw[2 * k] = a.x; xw[2 * k + 1] = a.y;
+            const int col = 2 * tx - R + 2 * k, row = r0 + r;
+            woff[r][k] = col < 0 ? L::CENTER + row * R + (col + R)
+                       : col >= TX ? L::CENTER + L::STRIP + row * R + (col - TX)
+                                   : (R + row) * TX + col;
         }
-        double lx[2], ly[2], lz[2];
+    const int crow0 = (R + r0) * TX + 2 * tx;   // tile offset of (row r0, column 2tx)
+
+    // lap at the 4 points from a tile (x, y) and a queue (z): same sums in the same order as
+    // the single-step kernel; the y neighbours are streamed so rows r0 and r0+1 share loads
+    auto lap4 = [&](const double* tile, const double (*q)[4], double* lap, double* cen) {
+        double lx[4], ly[4], lz[4];
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            centre[v] = xw[R + v];
-            lx[v] = FD<R>::b0() * xw[R + v]; ly[v] = lx[v]; lz[v] = lx[v];
-        }
+        for (int r = 0; r < 2; ++r) {
+            double xw[2 * R + 2];
 #pragma unroll
-        for (int j = 1; j <= R; ++j) {
-            const double2 up = *reinterpret_cast<const double2*>(tile + crow - j * TX);
-            const double2 dn = *reinterpret_cast<const double2*>(tile + crow + j * TX);
-            const double upv[2] = {up.x, up.y}, dnv[2] = {dn.x, dn.y};
+            for (int k = 0; k <= R; ++k) {
+                const double2 a = *reinterpret_cast<const double2*>(tile + woff[r][k]);
+                xw[2 * k] = a.x; xw[2 * k + 1] = a.y;
+            }
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-                lx[v] = fma(FD<R>::b(j), xw[R + v + j] + xw[R + v - j], lx[v]);
-                ly[v] = fma(FD<R>::b(j), dnv[v] + upv[v], ly[v]);
-                lz[v] = fma(FD<R>::b(j), q[R + j].v[v] + q[R - j].v[v], lz[v]);
+                const int p = 2 * r + v;
+                cen[p] = xw[R + v];
+                lx[p] = FD<R>::b0() * xw[R + v];
+#pragma unroll
+                for (int j = 1; j <= R; ++j) lx[p] = fma(FD<R>::b(j), xw[R + v + j] + xw[R + v - j], lx[p]);
+                ly[p] = FD<R>::b0() * xw[R + v];
+                lz[p] = ly[p];
+            }
+        }
+        double prev_up[2], prev_dn[2];          // rows r0-(j-1) and r0+j of the previous j
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            const double2 u = *reinterpret_cast<const double2*>(tile + crow0 - j * TX);          // r0 - j
+            const double2 d = *reinterpret_cast<const double2*>(tile + crow0 + (1 + j) * TX);    // r0+1+j
+            const double up0[2] = {u.x, u.y}, dn1[2] = {d.x, d.y};
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const double dn0 = (j == 1) ? cen[2 + v] : prev_dn[v];     // row r0 + j
+                const double up1 = (j == 1) ? cen[v] : prev_up[v];         // row r0 + 1 - j
+                ly[v] = fma(FD<R>::b(j), dn0 + up0[v], ly[v]);
+                ly[2 + v] = fma(FD<R>::b(j), dn1[v] + up1, ly[2 + v]);
+                prev_up[v] = up0[v];
+                prev_dn[v] = dn1[v];
             }
         }
 #pragma unroll
-        for (int v = 0; v < 2; ++v) lap[v] = fma(A.sx2, lx[v], fma(A.sy2, ly[v], A.sz2 * lz[v]));
+        for (int p = 0; p < 4; ++p) {
+#pragma unroll
+            for (int j = 1; j <= R; ++j) lz[p] = fma(FD<R>::b(j), q[R + j][p] + q[R - j][p], lz[p]);
+            lap[p] = fma(A.sx2, lx[p], fma(A.sy2, ly[p], A.sz2 * lz[p]));
+        }
     };
 
     bool bad = false;
@@ -229,58 +260,62 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         if (producer && i + D - 1 < niter) issue_stage(i + D - 1);
         mbar_wait(&full[s], (uint32_t)((i / D) & 1));
         const double* st = stages + (size_t)s * STAGE;
-        V csv, cpv, cau, cav;                                    // own points of plane z
-        {
-            const double* pw = st + 3 * TILE + ty * TX + 2 * tx;
-            const double2 a = *reinterpret_cast<const double2*>(pw + L::PWT);
-            const double2 b = *reinterpret_cast<const double2*>(pw + 2 * L::PWT);
-            csv.v[0] = a.x; csv.v[1] = a.y; cpv.v[0] = b.x; cpv.v[1] = b.y;
-            cau.v[0] = cau.v[1] = cav.v[0] = cav.v[1] = 0.0;
+        if (i + R < niter) build(st + TILE, st + 2 * TILE, i + R);   // u_a tile of plane z+R
+        double csv[4], cpv[4], cau[4] = {0, 0, 0, 0}, cav[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int po = (r0 + r) * TX + 2 * tx;                      // own column in a centre box
+            const int to = (R + r0 + r) * TX + 2 * tx;                  // own column in a tile
+            const double2 fs = *reinterpret_cast<const double2*>(st + 3 * TILE + po);
+            const double2 fv = *reinterpret_cast<const double2*>(st + TILE + to);
+            const double2 fp = *reinterpret_cast<const double2*>(st + 2 * TILE + to);
+            qs[2 * R][2 * r] = fs.x; qs[2 * R][2 * r + 1] = fs.y;
+            qa[2 * R][2 * r] = fma(A.cfA, fv.x, fp.x);
+            qa[2 * R][2 * r + 1] = fma(A.cfA, fv.y, fp.y);
+            const double2 a = *reinterpret_cast<const double2*>(st + 3 * TILE + PWT + po);
+            const double2 b = *reinterpret_cast<const double2*>(st + 3 * TILE + 2 * PWT + po);
+            csv[2 * r] = a.x; csv[2 * r + 1] = a.y; cpv[2 * r] = b.x; cpv[2 * r + 1] = b.y;
             if constexpr (MODEB == MODE_FINACC) {
-                const double2 c = *reinterpret_cast<const double2*>(pw + 3 * L::PWT);
-                const double2 d = *reinterpret_cast<const double2*>(pw + 4 * L::PWT);
-                cau.v[0] = c.x; cau.v[1] = c.y; cav.v[0] = d.x; cav.v[1] = d.y;
+                const double2 c = *reinterpret_cast<const double2*>(st + 3 * TILE + 3 * PWT + po);
+                const double2 d = *reinterpret_cast<const double2*>(st + 3 * TILE + 4 * PWT + po);
+                cau[2 * r] = c.x; cau[2 * r + 1] = c.y; cav[2 * r] = d.x; cav[2 * r + 1] = d.y;
             }
         }
-        // the u_a tile of plane z+R, consumed R iterations from now
-        if (i + R < niter) build(st + TILE, st + 2 * TILE, i + R);
-        {   // queue fronts (plane z+R, own points)
-            const double2 fs = *reinterpret_cast<const double2*>(st + 3 * TILE + ty * TX + 2 * tx);
-            const double2 fv = *reinterpret_cast<const double2*>(st + TILE + crow);
-            const double2 fp = *reinterpret_cast<const double2*>(st + 2 * TILE + crow);
-            qs[2 * R].v[0] = fs.x; qs[2 * R].v[1] = fs.y;
-            qa[2 * R].v[0] = fma(A.cfA, fv.x, fp.x);
-            qa[2 * R].v[1] = fma(A.cfA, fv.y, fp.y);
-        }
-        double lapS[2], lapA[2], xs_c[2], xa_c[2];
-        laplacian(st, qs, lapS, xs_c);                          // S_u tile, plane z
+        double lapS[4], lapA[4], xs_c[4], xa_c[4];
+        lap4(st, qs, lapS, xs_c);                               // S_u tile, plane z
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);                  // stage s consumed by this warp
+        if (lane == 0) mbar_arrive(&empty[s]);
         {
             const int slot = i % RG;
             mbar_wait(&ua_full[slot], (uint32_t)((i / RG) & 1));
-            laplacian(ring + (size_t)slot * TILE, qa, lapA, xa_c);
+            lap4(ring + (size_t)slot * TILE, qa, lapA, xa_c);
             __syncwarp();
             if (lane == 0) mbar_arrive(&ua_empty[slot]);
         }
-        double ua[2], va[2], ub[2], vb[2];
+        double ua[4], va[4], ub[4], vb[4];
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            ua[v] = xa_c[v];                                                      // step A, u
-            va[v] = combine<MODE_LF>(cpv.v[v], csv.v[v], lapS[v], 0.0, A.cfA, 0.0);   // step A, v
-            ub[v] = combine<MODEB>(xs_c[v], ua[v], va[v], cau.v[v], A.cfB, A.wh);     // step B, u
-            vb[v] = combine<MODEB>(csv.v[v], va[v], lapA[v], cav.v[v], A.cfB, A.wh);  // step B, v
-            if constexpr (MODEB != MODE_LF) bad |= !isfinite(ub[v]) || !isfinite(vb[v]);
+        for (int p = 0; p < 4; ++p) {
+            ua[p] = xa_c[p];                                                    // step A, u
+            va[p] = combine<MODE_LF>(cpv[p], csv[p], lapS[p], 0.0, A.cfA, 0.0);     // step A, v
+            ub[p] = combine<MODEB>(xs_c[p], ua[p], va[p], cau[p], A.cfB, A.wh);     // step B, u
+            vb[p] = combine<MODEB>(csv[p], va[p], lapA[p], cav[p], A.cfB, A.wh);    // step B, v
+            if constexpr (MODEB != MODE_LF) bad |= !isfinite(ub[p]) || !isfinite(vb[p]);
         }
-        const int64_t o = zoff(z0 + i) + own;
-        if constexpr (MODEB == MODE_LF) {
-            *reinterpret_cast<double2*>(A.Au + o) = make_double2(ua[0], ua[1]);
-            *reinterpret_cast<double2*>(A.Av + o) = make_double2(va[0], va[1]);
-        }
-        *reinterpret_cast<double2*>(A.Bu + o) = make_double2(ub[0], ub[1]);
-        *reinterpret_cast<double2*>(A.Bv + o) = make_double2(vb[0], vb[1]);
+        const int64_t oz = zoff(z0 + i);
 #pragma unroll
-        for (int j = 0; j < 2 * R; ++j) { qs[j] = qs[j + 1]; qa[j] = qa[j + 1]; }
+        for (int r = 0; r < 2; ++r) {
+            const int64_t o = oz + own + (int64_t)r * nx;
+            if constexpr (MODEB == MODE_LF) {
+                *reinterpret_cast<double2*>(A.Au + o) = make_double2(ua[2 * r], ua[2 * r + 1]);
+                *reinterpret_cast<double2*>(A.Av + o) = make_double2(va[2 * r], va[2 * r + 1]);
+            }
+            *reinterpret_cast<double2*>(A.Bu + o) = make_double2(ub[2 * r], ub[2 * r + 1]);
+            *reinterpret_cast<double2*>(A.Bv + o) = make_double2(vb[2 * r], vb[2 * r + 1]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * R; ++j)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) { qs[j][p] = qs[j + 1][p]; qa[j][p] = qa[j + 1][p]; }
     }
     if constexpr (MODEB != MODE_LF)
         if (bad && A.nonfinite) *A.nonfinite = 1;

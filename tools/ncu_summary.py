@@ -42,7 +42,7 @@ def launches(path):
               f"share={tot[k] / T:.4f}")
 
 
-def full(path, traffic_cfg=None):
+def full(path, traffic_cfg=None, cls=0):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -57,7 +57,7 @@ def full(path, traffic_cfg=None):
         wr = float(d["dram__bytes_write.sum"]) * (1e9 if units[hdr.index("dram__bytes_write.sum")] == "Gbyte" else 1)
         print(f"  dram bytes per launch (read + write) = {rd + wr:.6g}")
         if traffic_cfg:
-            json.dump({"config": traffic_cfg, "lf_dram_bytes_per_launch": rd + wr,
+            json.dump({"config": traffic_cfg, "class": cls, "lf_dram_bytes_per_launch": rd + wr,
                        "source": os.path.basename(path), "kernel": d.get("Kernel Name")},
                       open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "profiles", "ncu_traffic.json"), "w"), indent=1)
@@ -78,4 +78,5 @@ if __name__ == "__main__":
         launches(sys.argv[2])
     else:
         cfg = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
-        full(sys.argv[2], cfg)
+        cls = int(sys.argv[sys.argv.index("--class") + 1]) if "--class" in sys.argv else 0
+        full(sys.argv[2], cfg, cls)
