@@ -18,7 +18,8 @@ Recipes (draw order is part of the recipe; ``numpy.random.default_rng(seed)``):
   space (kx > 0) or (kx = 0, ky > 0) or (kx = ky = 0, kz > 0), enumerated in
   ascending lexicographic (kz, ky, kx) order; one phase phi_k ~ U[0, 2*pi)
   per mode in that order; field = sum_k |k|^-2 cos(2*pi k.x + phi_k)
-  (a real, i.e. Hermitian-symmetric, band-limited field), scaled to unit RMS.
+  (a real, i.e. Hermitian-symmetric, band-limited field), divided by its exact RMS
+  sqrt(sum_k |k|^-4 / 2) (Parseval), i.e. unit RMS.
   Placed in p (2-D acoustics, u = v = 0) or in u (3-D wave, v = 0).
 """
 
@@ -60,17 +61,18 @@ def gauss2d_sum8(nx: int, ny: int, seed: int) -> np.ndarray:
     return out
 
 
-def gauss3d(nx: int, ny: int, nz: int, seed: int) -> np.ndarray:
+def gauss3d(nx: int, ny: int, nz: int, seed: int, srange=None) -> np.ndarray:
     rng = np.random.default_rng(seed)
     cx, cy, cz = rng.uniform(0.3, 0.7, size=3)
     s = rng.uniform(0.03, 0.08)
     gx = np.exp(-(_min_image(_axis(nx), cx) / s) ** 2)
     gy = np.exp(-(_min_image(_axis(ny), cy) / s) ** 2)
     gz = np.exp(-(_min_image(_axis(nz), cz) / s) ** 2)
-    out = np.zeros((2, nz, ny, nx), dtype=np.float64)
+    lo, hi = (0, nz) if srange is None else srange
+    out = np.zeros((2, hi - lo, ny, nx), dtype=np.float64)
     gyx = gy[:, None] * gx[None, :]
-    for z in range(nz):
-        out[0, z] = gz[z] * gyx
+    for z in range(lo, hi):
+        out[0, z - lo] = gz[z] * gyx
     return out
 
 
@@ -92,38 +94,47 @@ def _half_space_modes(dims: tuple, kmax: int = KMAX):
     return np.array(modes, dtype=np.int64).reshape(-1, 3), lim
 
 
-def bandlimited(dims: tuple, seed: int) -> np.ndarray:
+def bandlimited(dims: tuple, seed: int, srange=None) -> np.ndarray:
     """Real band-limited field on the grid `dims` = (nx[, ny[, nz]]), unit RMS.
 
     Evaluated as Re(sum_k A_k e^{i phi_k} e^{2 pi i k.x}) by staged inverse
-    transforms (z, y by small dense matrices; x by a real inverse FFT).
+    transforms (z, y by small dense matrices; x by a real inverse FFT) and scaled by
+    the exact RMS sqrt(sum_k A_k^2 / 2) (Parseval: the half-space modes are distinct,
+    none is a Nyquist mode).  `srange` = (lo, hi) returns only planes [lo, hi) of the
+    slowest axis (z in 3-D, y in 2-D), identical to the same planes of the full field.
     """
     rng = np.random.default_rng(seed)
     modes, lim = _half_space_modes(dims)
     phase = rng.uniform(0.0, 2.0 * np.pi, size=len(modes))
     amp = 1.0 / (modes ** 2).sum(axis=1).astype(np.float64)   # |k|^-2
     coef = amp * np.exp(1j * phase)
+    rms = np.sqrt(0.5 * np.sum(amp * amp))
     nd = len(dims)
     nx = dims[0]
     ny = dims[1] if nd >= 2 else 1
     nz = dims[2] if nd == 3 else 1
+    slow = nz if nd == 3 else ny
+    lo, hi = (0, slow) if srange is None else (int(srange[0]), int(srange[1]))
     Kx, Ky, Kz = lim[0], (lim[1] if nd >= 2 else 0), (lim[2] if nd == 3 else 0)
     T = np.zeros((2 * Kz + 1, 2 * Ky + 1, Kx + 1), dtype=np.complex128)
     T[modes[:, 2] + Kz, modes[:, 1] + Ky, modes[:, 0]] = coef
     # irfft convention: f(x) = nx * irfft(G')[x], G'_0 = G_0, G'_k = G_k / 2
     T[:, :, 1:] *= 0.5
-    Ez = np.exp(2j * np.pi * np.outer(np.arange(nz), np.arange(-Kz, Kz + 1)) / nz)
-    Ey = np.exp(2j * np.pi * np.outer(np.arange(ny), np.arange(-Ky, Ky + 1)) / ny)
-    Tz = np.tensordot(Ez, T, axes=([1], [0]))          # (nz, 2Ky+1, Kx+1)
-    out = np.empty((nz, ny, nx), dtype=np.float64)
-    chunk = max(1, (1 << 26) // max(1, ny * (nx // 2 + 1)))
-    for z0 in range(0, nz, chunk):
-        z1 = min(nz, z0 + chunk)
-        G = np.matmul(Ey[None, :, :], Tz[z0:z1])          # (zc, ny, Kx+1)
-        Gp = np.zeros((z1 - z0, ny, nx // 2 + 1), dtype=np.complex128)
+    zs = np.arange(lo, hi) if nd == 3 else np.arange(1)
+    ys = np.arange(ny) if nd == 3 else np.arange(lo, hi)
+    Ez = np.exp(2j * np.pi * np.outer(zs, np.arange(-Kz, Kz + 1)) / nz)
+    Ey = np.exp(2j * np.pi * np.outer(ys, np.arange(-Ky, Ky + 1)) / ny)
+    # one plane at a time, so a plane's bytes do not depend on the requested range
+    T2 = T.reshape(T.shape[0], -1)
+    Tz = np.stack([(Ez[i:i + 1] @ T2).reshape(T.shape[1:]) for i in range(len(zs))])   # (nzr, 2Ky+1, Kx+1)
+    out = np.empty((len(zs), len(ys), nx), dtype=np.float64)
+    chunk = max(1, (1 << 26) // max(1, len(ys) * (nx // 2 + 1)))
+    for z0 in range(0, len(zs), chunk):
+        z1 = min(len(zs), z0 + chunk)
+        G = np.matmul(Ey[None, :, :], Tz[z0:z1])          # (zc, nyr, Kx+1)
+        Gp = np.zeros((z1 - z0, len(ys), nx // 2 + 1), dtype=np.complex128)
         Gp[:, :, : Kx + 1] = G
         out[z0:z1] = nx * np.fft.irfft(Gp, n=nx, axis=2)
-    rms = np.sqrt(np.mean(out * out))
     out /= rms
     if nd == 1:
         return out[0, 0]
@@ -132,22 +143,32 @@ def bandlimited(dims: tuple, seed: int) -> np.ndarray:
     return out
 
 
-def make_ic(w: Workload) -> np.ndarray:
-    """Initial state for workload `w`, shaped ``w.state_shape``, float64."""
+def make_ic(w: Workload, srange=None) -> np.ndarray:
+    """Initial state for workload `w`, shaped ``w.state_shape``, float64.
+
+    `srange` = (lo, hi): only planes [lo, hi) of the slowest axis (z in 3-D, y in 2-D),
+    bit-identical to the same planes of the full state (for multi-GPU slabs)."""
     nx, ny, nz = w.n
+    if srange is not None and w.ndim == 1:
+        raise ValueError("1-D states are not slabbed")
     if w.ic == "gauss1d":
         y = gauss1d(nx, w.seed)
     elif w.ic == "gauss2d_sum8":
         y = gauss2d_sum8(nx, ny, w.seed)
+        if srange is not None:
+            y = y[:, srange[0]:srange[1]]
     elif w.ic == "gauss3d":
-        y = gauss3d(nx, ny, nz, w.seed)
+        y = gauss3d(nx, ny, nz, w.seed, srange)
     elif w.ic == "bandlimited2d":
-        y = np.zeros((3, ny, nx), dtype=np.float64)
-        y[0] = bandlimited((nx, ny), w.seed)
+        p = bandlimited((nx, ny), w.seed, srange)
+        y = np.zeros((3,) + p.shape, dtype=np.float64)
+        y[0] = p
     elif w.ic == "bandlimited3d":
-        y = np.zeros((2, nz, ny, nx), dtype=np.float64)
-        y[0] = bandlimited((nx, ny, nz), w.seed)
+        u = bandlimited((nx, ny, nz), w.seed, srange)
+        y = np.zeros((2,) + u.shape, dtype=np.float64)
+        y[0] = u
     else:
         raise ValueError(f"unknown IC recipe {w.ic!r}")
-    assert y.shape == w.state_shape, (y.shape, w.state_shape)
+    if srange is None:
+        assert y.shape == w.state_shape, (y.shape, w.state_shape)
     return np.ascontiguousarray(y, dtype=np.float64)

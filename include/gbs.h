@@ -178,6 +178,14 @@ GBS_API int gbs_advance(gbs_ctx* ctx, int64_t macro_steps, double H);
  * the full grid (slabs are all-gathered). */
 GBS_API int gbs_read_state(gbs_ctx* ctx, double* dst, int64_t count, int on_device);
 
+/* Slab-local IO for multi-GPU callers that hold only their own part of the grid:
+ * src/dst hold this rank's planes [slab_z0, slab_z0 + slab_nz) of the slowest axis
+ * (gbs_query / gbs_plan) for every field, SoA [F][slab_nz][...], count = F * slab_nz *
+ * plane.  Single GPU: the slab is the whole grid (identical to the full-grid calls).
+ * gbs_read_slab synchronizes and surfaces deferred errors like gbs_read_state. */
+GBS_API int gbs_write_slab(gbs_ctx* ctx, const double* src, int64_t count, int on_device);
+GBS_API int gbs_read_slab(gbs_ctx* ctx, double* dst, int64_t count, int on_device);
+
 /* Wait for all queued work; surfaces deferred errors. */
 GBS_API int gbs_sync(gbs_ctx* ctx);
 

@@ -1174,6 +1174,51 @@ int gbs_read_state(gbs_ctx* c, double* dst, int64_t count, int on_device) {
     return harvest_timer(c);
 }
 
+// this rank's planes [z_lo, z_lo + nz_rank) of the slowest axis (all its local slabs)
+static void rank_planes(const gbs_ctx* c, int64_t* z_lo, int64_t* nz_rank) {
+    *z_lo = c->slab[0].z0;
+    *nz_rank = 0;
+    for (const auto& s : c->slab) *nz_rank += s.nz;
+}
+
+int gbs_write_slab(gbs_ctx* c, const double* src, int64_t count, int on_device) {
+    if (!c || !src) return fail(c, GBS_E_INVAL, "ctx or src is NULL");
+    int64_t z_lo, nzr;
+    rank_planes(c, &z_lo, &nzr);
+    const int64_t per_field = nzr * c->plane;
+    if (count != c->F * per_field)
+        return fail(c, GBS_E_INVAL, "count=%lld, expected F*slab points=%lld", (long long)count,
+                    (long long)(c->F * per_field));
+    CU(c, cudaSetDevice(c->device));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (auto& s : c->slab)
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(field_ptr(c, s, c->yb, f), src + (int64_t)f * per_field + (s.z0 - z_lo) * c->plane,
+                                  sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
+    c->have_state = true;
+    return GBS_OK;
+}
+
+int gbs_read_slab(gbs_ctx* c, double* dst, int64_t count, int on_device) {
+    if (!c || !dst) return fail(c, GBS_E_INVAL, "ctx or dst is NULL");
+    if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_read_slab before gbs_write_state/slab");
+    int64_t z_lo, nzr;
+    rank_planes(c, &z_lo, &nzr);
+    const int64_t per_field = nzr * c->plane;
+    if (count != c->F * per_field)
+        return fail(c, GBS_E_INVAL, "count=%lld, expected F*slab points=%lld", (long long)count,
+                    (long long)(c->F * per_field));
+    CU(c, cudaSetDevice(c->device));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    for (auto& s : c->slab)
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(dst + (int64_t)f * per_field + (s.z0 - z_lo) * c->plane, field_ptr(c, s, c->yb, f),
+                                  sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
+    int rc = gbs_sync(c);
+    if (rc) return rc;
+    return harvest_timer(c);
+}
+
 int gbs_query(const gbs_ctx* c, gbs_info* info) {
     if (!c || !info) return fail(const_cast<gbs_ctx*>(c), GBS_E_INVAL, "ctx or info is NULL");
     memset(info, 0, sizeof(*info));

@@ -25,7 +25,8 @@ PDE = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
 FIELDS = {"adv1d": 1, "acoustic2d": 3, "wave3d": 2}
 NDIM = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
 
-EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_sync",
+EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_write_slab",
+           "gbs_read_slab", "gbs_sync",
            "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
            "gbs_set_option",
            "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
@@ -106,6 +107,8 @@ def load(build_if_missing: bool = False):
     L.gbs_write_state.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_advance.argtypes = [vp, i64, ctypes.c_double]
     L.gbs_read_state.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_write_slab.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_read_slab.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_sync.argtypes = [vp]
     L.gbs_destroy.argtypes = [vp]
     L.gbs_destroy.restype = None
@@ -225,6 +228,16 @@ def gbs_read_state(ctx, dst) -> None:
     _check(load().gbs_read_state(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
 
 
+def gbs_write_slab(ctx, src) -> None:
+    p, dev, cnt = _ptr_and_device(src)
+    _check(load().gbs_write_slab(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
+
+
+def gbs_read_slab(ctx, dst) -> None:
+    p, dev, cnt = _ptr_and_device(dst)
+    _check(load().gbs_read_slab(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
+
+
 def gbs_sync(ctx) -> None:
     _check(load().gbs_sync(ctx), ctx)
 
@@ -276,6 +289,13 @@ class Stepper:
 
     def read(self, out):
         gbs_read_state(self.ctx, out)
+        return out
+
+    def write_slab(self, y):
+        gbs_write_slab(self.ctx, y)
+
+    def read_slab(self, out):
+        gbs_read_slab(self.ctx, out)
         return out
 
     def info(self):

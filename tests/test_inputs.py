@@ -51,3 +51,14 @@ def test_gauss1d_recipe():
     i = int(np.argmax(u))
     assert abs(i / 256 - c) <= 1 / 256 and u.max() <= 1.0
     assert 0.3 <= c <= 0.7 and 0.03 <= s <= 0.08
+
+
+@pytest.mark.parametrize("name,n", [("c2", (48, 40, 1)), ("c3", (96, 80, 1)), ("c4", (40, 36, 32)),
+                                    ("c5", (64, 48, 40))])
+def test_slab_ic_equals_planes_of_full_ic(name, n):
+    """Multi-GPU ranks generate only their slab; the bytes must equal the full IC's planes."""
+    w = reduced(name, n)
+    full = make_ic(w)
+    slow = n[2] if w.ndim == 3 else n[1]
+    parts = [make_ic(w, (a, min(a + 13, slow))) for a in range(0, slow, 13)]
+    assert np.array_equal(np.concatenate(parts, axis=1), full)

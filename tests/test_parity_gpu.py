@@ -218,6 +218,28 @@ def test_host_buffers_match_device_buffers(torch_cuda):
     assert np.array_equal(gd[0], gh[0])
 
 
+def test_slab_io_round_trip(torch_cuda):
+    """gbs_write_slab / gbs_read_slab (one GPU: the slab is the whole grid, also with
+    loopback slabs) move the same bytes as the full-grid calls."""
+    gbs = gbs_mod()
+    torch = torch_cuda
+    w = reduced("c4", (64, 32, 24), macro_steps=1, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0 = make_ic(w)
+    outs = []
+    for lb in (1, 3):
+        with gbs.Stepper(w.pde, w.n, w.order, counts, wd, loopback=lb) as st:
+            st.write_slab(torch.from_numpy(y0).cuda())
+            st.advance(1, H)
+            a = torch.empty(y0.shape, dtype=torch.float64, device="cuda")
+            b = np.empty_like(y0)
+            st.read_slab(a)
+            st.read(b)
+            assert np.array_equal(a.cpu().numpy(), b)
+            outs.append(b)
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_graph_replay_is_bitwise_identical(torch_cuda):
     w = reduced("c4", (40, 36, 34), macro_steps=3, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8")
