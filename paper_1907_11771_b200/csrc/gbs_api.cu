@@ -341,11 +341,14 @@ static void free_state(gbs_ctx* c) {
 // ---------------------------------------------------------------------------
 // kernel dispatch
 // ---------------------------------------------------------------------------
+struct Slot { int b, f; };   // one field of one state buffer
 struct StepOperands {
-    int S, P, O;          // buffer indices (0..3) of the current level, previous level, output
+    int S, P, O;          // buffer indices of the current level, previous level, output
     int mode;
     double cf, wh;
     bool flag;
+    Slot xu = {-1, 0};    // FE only (TMA kernel): also write u_2 = S_u + cf2 v_1 here
+    double cf2 = 0.0;
 };
 
 template <int R, int MODE, bool SLAB>
@@ -410,6 +413,8 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
         a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
         a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        a.Xu = op.xu.b >= 0 ? field_ptr(c, s, op.xu.b, op.xu.f) : nullptr;
+        a.cf2 = op.cf2;
         const bool vx2 = (c->n[0] % 2) == 0;
         if (c->use_bulk && s.tma_ok) {
             int64_t tx = c->n[0] / gbs::tma::TX, ty = c->n[1] / gbs::tma::TY;
@@ -501,11 +506,14 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
     return GBS_OK;
 }
 
-// Two consecutive substeps of one sequence in one launch (3-D wave, TMA grids):
-// step A = LF from (P, S); step B = LF (writes OA = y_{n+1}, OB = y_{n+2}) or the
-// fused final step (modeB = FIN0/FINACC, writes the accumulator OB only).
+// Two consecutive substeps of one sequence in one launch (3-D wave, TMA grids),
+// gbs_wave3d_pair.cuh.  Operands are field slots (buffer, field): the pair
+// kernel reads P_v, S = (S_u, S_v) and U = u_{n+1}; LF writes Av = v_{n+1},
+// (Bu, Bv) = y_{n+2} and Cu = u_{n+3}; FIN0/FINACC writes the accumulator
+// buffer's two fields only.
 struct PairOperands {
-    int P, S, OA, OB;
+    Slot Pv, Su, Sv, U;
+    Slot Av, Bu, Bv, Cu;          // LF outputs (Bu.b = the accumulator buffer for FIN)
     int modeB;
     double cfA, cfB, wh;
     bool flag;
@@ -513,11 +521,18 @@ struct PairOperands {
 
 static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
     const bool slab = c->ghost > 0;
+    const bool lf = op.modeB == gbs::MODE_LF;
     gbs::tma::PairArgs a;
-    a.Au = field_ptr(c, s, op.OA, 0); a.Av = field_ptr(c, s, op.OA, 1);
-    a.Bu = field_ptr(c, s, op.OB, 0); a.Bv = field_ptr(c, s, op.OB, 1);
-    a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1);
-    a.Pu = field_ptr(c, s, op.P, 0); a.Pv = field_ptr(c, s, op.P, 1);
+    if (lf) {
+        a.Av = field_ptr(c, s, op.Av.b, op.Av.f);
+        a.Bu = field_ptr(c, s, op.Bu.b, op.Bu.f); a.Bv = field_ptr(c, s, op.Bv.b, op.Bv.f);
+        a.Cu = field_ptr(c, s, op.Cu.b, op.Cu.f);
+    } else {
+        a.Av = a.Cu = nullptr;
+        a.Bu = field_ptr(c, s, op.Bu.b, 0); a.Bv = field_ptr(c, s, op.Bu.b, 1);
+    }
+    a.Su = field_ptr(c, s, op.Su.b, op.Su.f);
+    a.U = field_ptr(c, s, op.U.b, op.U.f);
     a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
     a.plane = c->plane;
     const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
@@ -528,11 +543,11 @@ static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
     dim3 grid((unsigned)(c->n[0] / gbs::tma::TX), (unsigned)(c->n[1] / gbs::tma::TY),
               (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
     gbs::tma::PairMaps m;
-    m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
-    m.sv_a = s.tm[op.S][1][0]; m.sv_b = s.tm[op.S][1][1]; m.sv_c = s.tm[op.S][1][2];
-    m.pu_a = s.tm[op.P][0][0]; m.pu_b = s.tm[op.P][0][1]; m.pu_c = s.tm[op.P][0][2];
-    m.pv = s.tm[op.P][1][0];
-    m.acc_u = s.tm[op.OB][0][0]; m.acc_v = s.tm[op.OB][1][0];
+    m.su_a = s.tm[op.Su.b][op.Su.f][0]; m.su_b = s.tm[op.Su.b][op.Su.f][1]; m.su_c = s.tm[op.Su.b][op.Su.f][2];
+    m.u_a = s.tm[op.U.b][op.U.f][0]; m.u_b = s.tm[op.U.b][op.U.f][1]; m.u_c = s.tm[op.U.b][op.U.f][2];
+    m.sv = s.tm[op.Sv.b][op.Sv.f][0];
+    m.pv = s.tm[op.Pv.b][op.Pv.f][0];
+    m.acc_u = s.tm[op.Bu.b][0][0]; m.acc_v = s.tm[op.Bu.b][1][0];
     const int zbase = (int)c->ghost;
     cudaError_t e = cudaSuccess;
 #define PR(RR, SL)                                                                                          \
@@ -664,9 +679,9 @@ static int step(gbs_ctx* c, int cls, const StepOperands& op) {
 
 static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
     int rc;
-    // the pair kernel reads S_u, S_v and P_u with stencils
-    if ((rc = exchange_halo(c, op.S, 0x3u))) return rc;
-    if ((rc = exchange_halo(c, op.P, 0x1u))) return rc;
+    // the pair kernel reads S_u and U with stencils
+    if ((rc = exchange_halo(c, op.Su.b, 1u << op.Su.f))) return rc;
+    if ((rc = exchange_halo(c, op.U.b, 1u << op.U.f))) return rc;
     cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
     for (auto& s : c->slab)
@@ -712,24 +727,26 @@ static int enqueue_macro(gbs_ctx* c, double H) {
         const double h = H / (double)n;
         const bool last = (q + 1 == c->my_seq.size());
         if (fused) {
-            // FE, then n/2 launches of two substeps: (LF1,LF2), ..., (LF_{n-1}, final)
-            const int L0 = 2;
-            if ((rc = step(c, 1, {Y, Y, L0, gbs::MODE_FE, h, 0.0, false}))) return rc;      // y1
-            int prev = Y, cur = L0;
+            // FE (which also forms u_2), then n/2 launches of two substeps:
+            // (LF1, LF2), ..., (LF_{n-1}, final).  Field slots: y1 -> buffer 2; the
+            // u-levels rotate through (2,0)/(3,0) and (4,0)/(5,0); v_{odd} stays in
+            // (2,1) and v_{even} in (3,1), both updated in place (pointwise reads).
+            StepOperands fe{Y, Y, 2, gbs::MODE_FE, h, 0.0, false};
+            fe.xu = Slot{3, 0};
+            fe.cf2 = 2.0 * h;
+            if ((rc = step(c, 1, fe))) return rc;                                            // y1, u2
+            Slot Pv{Y, 1}, Su{2, 0}, Sv{2, 1}, U{3, 0};
             for (int p = 0; p < n / 2; ++p) {
                 if (p + 1 < n / 2) {
-                    int outs[2], no = 0;
-                    for (int b = 2; b < 6 && no < 2; ++b)
-                        if (b != prev && b != cur) outs[no++] = b;
-                    if ((rc = pair_step(c, 3, {prev, cur, outs[0], outs[1], gbs::MODE_LF, 2.0 * h, 2.0 * h, 0.0,
-                                               false})))
-                        return rc;
-                    prev = outs[0];
-                    cur = outs[1];
+                    const int nb = Su.b == 2 ? 4 : 2;
+                    PairOperands op{Pv, Su, Sv, U, Slot{3, 1}, Slot{nb, 0}, Sv, Slot{nb + 1, 0},
+                                    gbs::MODE_LF, 2.0 * h, 2.0 * h, 0.0, false};
+                    if ((rc = pair_step(c, 3, op))) return rc;
+                    Pv = Slot{3, 1}; Su = Slot{nb, 0}; U = Slot{nb + 1, 0};
                 } else {
-                    PairOperands fin{prev, cur, -1, ACC, first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, 2.0 * h, h,
+                    PairOperands fin{Pv, Su, Sv, U, Slot{ACC, 0}, Slot{ACC, 0}, Slot{ACC, 1}, Slot{ACC, 0},
+                                     first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, 2.0 * h, h,
                                      0.5 * c->wk_all[k], last};
-                    fin.OA = ACC;     // unused by the FIN modes
                     if ((rc = pair_step(c, 4, fin))) return rc;
                 }
             }

@@ -109,6 +109,8 @@ struct Wave3DArgs {
     double sx2, sy2, sz2;    // squared inverse spacings
     double cf, wh;
     int* nonfinite;          // optional flag (FIN modes)
+    double* Xu;              // optional (FE, TMA kernel): u_2 = S_u + cf2 * v_1, the first
+    double cf2;              // leap-frog step's u-component, for the two-substep kernel
 };
 
 template <int R, int MODE, int VX, int BY, bool SLAB>

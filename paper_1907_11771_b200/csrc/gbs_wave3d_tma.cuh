@@ -252,6 +252,14 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
         const int64_t o = zoff(z0 + i) + own;
         *reinterpret_cast<double2*>(A.Ou + o) = make_double2(ou[0], ou[1]);
         *reinterpret_cast<double2*>(A.Ov + o) = make_double2(ov[0], ov[1]);
+        if constexpr (MODE == MODE_FE) {
+            // u_2 = u_0 + 2h v_1 (the next leap-frog step's pointwise u, formed exactly as
+            // the single-step LF kernel forms it) for the two-substep kernel
+            if (A.Xu)
+                *reinterpret_cast<double2*>(A.Xu + o) =
+                    make_double2(combine<MODE_LF>(xw[R], 0.0, ov[0], 0.0, A.cf2, 0.0),
+                                 combine<MODE_LF>(xw[R + 1], 0.0, ov[1], 0.0, A.cf2, 0.0));
+        }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j) q[j] = q[j + 1];
     }
