@@ -3,6 +3,7 @@ metrics of a --set full capture (run here, on the CPU box, with `ncu -i`).
 
     python tools/ncu_summary.py launches <launches.csv>            > profiles/rNN_launch_shares.txt
     python tools/ncu_summary.py full <prof.ncu-rep> [--traffic CFG] > profiles/rNN_ncu_<kernel>.txt
+    python tools/ncu_summary.py stalls <prof.ncu-rep>                > profiles/rNN_ncu_<kernel>_stalls.txt
 """
 import csv
 import io
@@ -73,9 +74,40 @@ def full(path, traffic_cfg=None, cls=0):
             print(f"  {r[si][:28]:28s} {r[mi][:52]:52s} {r[vi]:>16s} {r[ui]}")
 
 
+def stalls(path, top=10):
+    """Warp-stall sampling totals and the instructions with the most samples per reason
+    (source page, SASS view; needs --import-source / -lineinfo)."""
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(src)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    hdr, data = rows[hi], rows[hi + 1:]
+
+    def num(x):
+        try:
+            return float(x)
+        except ValueError:
+            return 0.0
+    si = hdr.index("Warp Stall Sampling (All Samples)")
+    total = sum(num(r[si]) for r in data)
+    cols = [(i, h) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    print(f"# warp-stall samples ({os.path.basename(path)}, {rows[0][1] if len(rows[0]) > 1 else ''}): "
+          f"{total:.0f} samples")
+    sums = sorted(((sum(num(r[i]) for r in data), h, i) for i, h in cols), reverse=True)
+    for v, h, _ in sums:
+        if v > 0:
+            print(f"  {h:28s} {v:10.0f}  {v / total:6.1%}")
+    for v, h, i in sums[:4]:
+        print(f"# top instructions by {h}")
+        for r in sorted(data, key=lambda r: -num(r[i]))[:top]:
+            print(f"  {r[0][-6:]} {num(r[i]):9.0f}  {r[1].strip()[:90]}")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "stalls":
+        stalls(sys.argv[2])
     else:
         cfg = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
         cls = int(sys.argv[sys.argv.index("--class") + 1]) if "--class" in sys.argv else 0

@@ -12,6 +12,7 @@ ap.add_argument("--macro", type=int, default=2)
 ap.add_argument("--zchunk", type=int, default=0)
 ap.add_argument("--n", type=str, default="")
 ap.add_argument("--fuse", type=int, default=-1)
+ap.add_argument("--opt", action="append", default=[], help="key=value (gbs_set_option)")
 a = ap.parse_args()
 w = get_config(a.config)
 if a.n:
@@ -25,6 +26,10 @@ torch.cuda.set_stream(stream)
 st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, stream=stream.cuda_stream)
 if a.zchunk: gbs.gbs_set_option(st.ctx, "zchunk", a.zchunk)
 if a.fuse >= 0: gbs.gbs_set_option(st.ctx, "fuse", a.fuse)
+for kv in a.opt:
+    k, v = kv.split("="); gbs.gbs_set_option(st.ctx, k, int(v))
+res_opts = dict(kv.split("=") for kv in a.opt)
+if os.environ.get("GBS_PAD"): res_opts["GBS_PAD"] = os.environ["GBS_PAD"]
 st.write(y0)
 st.advance(1, H); gbs.gbs_sync(st.ctx)
 gbs.gbs_set_option(st.ctx, "time_kernels", 1)
@@ -34,7 +39,7 @@ st.advance(a.macro, H)
 t1.record(stream); torch.cuda.synchronize(); gbs.gbs_sync(st.ctx)
 tot = t0.elapsed_time(t1)
 F = w.fields; pts = w.points
-res = {"config": w.name, "total_ms": tot, "macro": a.macro}
+res = {"config": w.name, "opts": res_opts, "total_ms": tot, "macro": a.macro}
 for cls, name in enumerate(["lf", "fe", "fin", "lf2", "lffin"]):
     ms, n = gbs.gbs_kernel_time(st.ctx, cls)
     if n == 0: continue
