@@ -254,6 +254,12 @@ def run_ours(a):
             3: ("two leap-frog substeps in one pass", 48 * F),
             4: ("leap-frog + final substep in one pass", 48 * F),
             5: ("whole-run cluster kernel", 24 * F * S * a.steps)}
+    # bytes per point the kernel itself must read + write once (its own minimum HBM
+    # traffic): the two-substep 3-D kernel moves S_u, U, S_v, P_v in and A_v, B, C_u out
+    # (gbs_wave3d_pair.cuh) = 64 B instead of the metric's 2 x 24F = 96 B, and the FE
+    # launch before it also writes u_2 (40 B); elsewhere it equals the metric's figure
+    fused3d = w.pde == "wave3d" and ktimes.get(3, (0, 0))[1] > 0
+    MOVED = {0: 24 * F, 1: 16 * F + (8 if fused3d else 0), 3: 64}
     dom = max(ktimes, key=lambda c: ktimes[c][0])
     dom_ms, dom_n = ktimes[dom]
     avg = dom_ms / max(dom_n, 1)
@@ -276,6 +282,12 @@ def run_ours(a):
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": KCLS[dom][0], "algorithmic_bytes_per_launch": alg,
                 "avg_launch_ms": round(avg, 4), "launches": dom_n, "peak_source": peak_src,
+                "algorithmic_bytes_note": ("SURVEY.md 8(d): 24F B per point per substep x substeps per launch; "
+                                           "a temporally blocked launch covers 2 substeps in one HBM pass, "
+                                           "so frac can exceed 1"),
+                "moved_bytes_per_launch": MOVED[dom] * local_pts if dom in MOVED else None,
+                "frac_of_moved": (round(MOVED[dom] * local_pts / (avg * 1e-3) / 1e9 / peak, 4)
+                                  if dom in MOVED else None),
                 "share_of_step": round(dom_ms / ms, 4) if ms > 0 else None,
                 "other_kernels": others}
 

@@ -18,6 +18,7 @@
 #include "gbs_kernels.cuh"
 #include "gbs_wave3d_tma.cuh"
 #include "gbs_wave3d_pair.cuh"
+#include "gbs_acoustic2d_tma.cuh"
 #include "gbs_adv1d_cluster.cuh"
 
 #include <cuda_runtime.h>
@@ -82,7 +83,7 @@ struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
     double* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // Y, ACC, L0..L3 (+ ghosts)
     bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
-    CUtensorMap tm[6][2][3];          // [buffer][field][box shape A/B/C] (wave3d)
+    CUtensorMap tm[6][3][3];          // [buffer][field][box shape A/B/C] (TMA kernels)
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -162,6 +163,7 @@ struct gbs_ctx {
     bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
     int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
+    int sms = 148;                    // streaming multiprocessors of the device
     int l2hint = 0;                   // pair kernel L2 eviction hints (gbs_wave3d_pair.cuh)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     double graph_H = -1.0;
@@ -299,8 +301,10 @@ static int alloc_state(gbs_ctx* c) {
     c->field_stride = (nzl + 2 * c->ghost) * c->plane;
     // the TMA (and two-substep) kernels need the grid to be a multiple of their tile so
     // halo boxes never cross the wrap; the two-substep kernels need 4 level buffers
-    c->tma_grid = c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0;
-    c->nbuf = c->tma_grid ? 6 : 4;
+    // (2-D acoustics: x a multiple of the tile width, each slab's rows a multiple of its height)
+    c->tma_grid = (c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0) ||
+                  (c->pde == GBS_ACOUSTIC2D && c->n[0] % gbs::tma::TX == 0 && nzl % gbs::tma::TY == 0);
+    c->nbuf = (c->tma_grid && c->pde == GBS_WAVE3D) ? 6 : 4;
     c->slab.resize(nloc);
     for (int v = 0; v < nloc; ++v) {
         Slab& s = c->slab[v];
@@ -318,12 +322,14 @@ static int alloc_state(gbs_ctx* c) {
         if (c->tma_grid) {
             bool ok = true;
             const int64_t dz = nzl + 2 * c->ghost;
+            // 3-D: views [dz][ny][nx]; 2-D: [1][ny_alloc][nx] (the slow axis is y)
+            const int64_t vy = c->pde == GBS_WAVE3D ? c->n[1] : dz, vz = c->pde == GBS_WAVE3D ? dz : 1;
             for (int b = 0; b < c->nbuf && ok; ++b)
-                for (int f = 0; f < 2 && ok; ++f) {
+                for (int f = 0; f < c->F && ok; ++f) {
                     double* base = s.buf[b] + (int64_t)f * c->field_stride;
-                    ok = make_map(&s.tm[b][f][0], base, c->n[0], c->n[1], dz, gbs::tma::TX, gbs::tma::TY) &&
-                         make_map(&s.tm[b][f][1], base, c->n[0], c->n[1], dz, gbs::tma::TX, c->R) &&
-                         make_map(&s.tm[b][f][2], base, c->n[0], c->n[1], dz, c->R, gbs::tma::TY);
+                    ok = make_map(&s.tm[b][f][0], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY) &&
+                         make_map(&s.tm[b][f][1], base, c->n[0], vy, vz, gbs::tma::TX, c->R) &&
+                         make_map(&s.tm[b][f][2], base, c->n[0], vy, vz, c->R, gbs::tma::TY);
                 }
             s.tma_ok = ok;
         }
@@ -385,6 +391,33 @@ static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::
     }
     gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY / 2), L::bytes, st>>>(m, a, zbase);
     return cudaSuccess;
+}
+template <int R, int MODE, bool SLAB>
+static cudaError_t launch_ac2d_tma(const gbs::tma::AcMaps& m, const gbs::Acoustic2DArgs& a, int ybase, dim3 grid,
+                                   cudaStream_t st) {
+    using L = gbs::tma::AcLayout<R, MODE>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::acoustic2d_step_tma<R, MODE, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gbs::tma::acoustic2d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, ybase);
+    return cudaSuccess;
+}
+// rows per CTA of the 2-D TMA kernel: a multiple of the tile height minimising
+// (waves of one-CTA-per-SM) x (rows + ~2 tiles of pipeline fill)
+static int ac2d_ychunk(int64_t xtiles, int64_t ny, int opt, int sms) {
+    const int T = gbs::tma::TY;
+    if (opt > 0) return (int)std::min<int64_t>(ny, ((opt + T - 1) / T) * T);
+    int64_t best = -1, bestc = T;
+    for (int64_t yc = T; yc <= ny; yc += T) {
+        const int64_t ctas = xtiles * ((ny + yc - 1) / yc);
+        const int64_t cost = ((ctas + sms - 1) / sms) * (yc + 2 * T);
+        if (best < 0 || cost < best) { best = cost; bestc = yc; }
+    }
+    return (int)bestc;
 }
 template <int R, int MODE, bool SLAB>
 static void launch_ac2d(const gbs::Acoustic2DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
@@ -470,6 +503,34 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         a.nx = (int)c->n[0]; a.ny = (int)s.nz;
         a.sx = c->n[0] / c->len[0]; a.sy = c->n[1] / c->len[1];
         a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        if (c->use_bulk && s.tma_ok) {
+            const int64_t xt = c->n[0] / gbs::tma::TX;
+            a.ychunk = ac2d_ychunk(xt, s.nz, c->zchunk_opt, c->sms);
+            dim3 grid((unsigned)xt, (unsigned)((s.nz + a.ychunk - 1) / a.ychunk));
+            gbs::tma::AcMaps m;
+            for (int f = 0; f < 3; ++f) {
+                m.s_a[f] = s.tm[op.S][f][0]; m.s_b[f] = s.tm[op.S][f][1]; m.s_c[f] = s.tm[op.S][f][2];
+                m.p[f] = s.tm[op.P][f][0];
+                m.acc[f] = s.tm[op.O][f][0];
+            }
+            const int ybase = (int)c->ghost;
+            cudaError_t e = cudaSuccess;
+#define A2B(RR, SL)                                                                                     \
+            switch (op.mode) {                                                                          \
+                case gbs::MODE_FE: e = launch_ac2d_tma<RR, gbs::MODE_FE, SL>(m, a, ybase, grid, c->stream); break;     \
+                case gbs::MODE_LF: e = launch_ac2d_tma<RR, gbs::MODE_LF, SL>(m, a, ybase, grid, c->stream); break;     \
+                case gbs::MODE_FIN0: e = launch_ac2d_tma<RR, gbs::MODE_FIN0, SL>(m, a, ybase, grid, c->stream); break; \
+                default: e = launch_ac2d_tma<RR, gbs::MODE_FINACC, SL>(m, a, ybase, grid, c->stream); break;           \
+            }
+            if (c->R == 2) { if (slab) { A2B(2, true) } else { A2B(2, false) } }
+            else { if (slab) { A2B(4, true) } else { A2B(4, false) } }
+#undef A2B
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "bulk kernel setup: %s", cudaGetErrorString(e));
+            c->launches++;
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return GBS_OK;
+        }
         const bool vx2 = (c->n[0] % 2) == 0;
         const int TX = vx2 ? 256 : 128;
         int64_t tx = (c->n[0] + TX - 1) / TX;
@@ -1033,6 +1094,8 @@ int gbs_create(const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, 
         return bail(fail(c, GBS_E_INVAL, "device %d out of range (%d devices)", c->device, ndev));
     if (cudaSetDevice(c->device) != cudaSuccess)
         return bail(fail(c, GBS_E_CUDA, "cudaSetDevice(%d) failed", c->device));
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (c->sms < 1) c->sms = 148;
     if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
     else {
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)

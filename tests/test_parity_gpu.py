@@ -113,6 +113,8 @@ CASES = [
     ("c2", (131, 90, 1), 3, "nonzero8"),           # odd nx -> 64-bit path
     ("c3", (264, 200, 1), 3, "nonzero8"),
     ("c3", (520, 72, 1), 2, "fallback8"),
+    ("c2", (128, 96, 1), 3, "nonzero8"),           # 2-D TMA kernel (multiple of the 64x16 tile)
+    ("c3", (192, 80, 1), 2, "nonzero8"),           # 2-D TMA kernel, FD8
     ("c4", (72, 40, 36), 2, "nonzero8"),           # ragged: 64-wide x tiles, 16-high y tiles
     ("c4", (72, 40, 36), 2, "fallback8"),
     ("c4", (65, 33, 40), 1, "nonzero8"),           # odd nx -> 64-bit path
@@ -129,6 +131,18 @@ def test_bulk_kernel_bitwise_equals_ldg_kernel(torch_cuda, n):
     register-prefetch kernel do the same arithmetic in the same order: results must
     agree bit for bit."""
     w = reduced("c4", n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"bulk": 1})
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"bulk": 0})
+    assert np.array_equal(a[0], b[0])
+
+
+@pytest.mark.parametrize("cfg,n", [("c2", (128, 64, 1)), ("c3", (64, 48, 1)), ("c3", (192, 80, 1)),
+                                   ("c2", (64, 16, 1))])
+def test_2d_bulk_kernel_bitwise_equals_register_kernel(torch_cuda, cfg, n):
+    """2-D acoustics: the TMA-pipelined kernel and the register y-march kernel do the
+    same arithmetic in the same order: bit-identical results."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8")
     _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"bulk": 1})
     _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"bulk": 0})
@@ -253,7 +267,8 @@ def test_graph_replay_is_bitwise_identical(torch_cuda):
 @pytest.mark.parametrize("cfg,n,slabs", [("c4", (40, 36, 32), 2), ("c4", (40, 36, 32), 4),
                                          ("c4", (128, 32, 36), 3), ("c5", (64, 32, 32), 4),
                                          ("c5", (36, 20, 24), 3), ("c2", (96, 64, 1), 4),
-                                         ("c3", (80, 48, 1), 3)])
+                                         ("c3", (80, 48, 1), 3), ("c2", (128, 64, 1), 4),
+                                         ("c3", (64, 96, 1), 3)])
 def test_loopback_slabs(torch_cuda, cfg, n, slabs):
     """z-slabs (y in 2-D) with ghost planes and halo copies, emulated on one GPU."""
     w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
