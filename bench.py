@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=0, help="sequence groups (0 = planner)")
+    ap.add_argument("--weights", default=None,
+                    help="weight set instead of the config's (e.g. opt8: the Appendix-B optimised "
+                         "weights on the config's step counts; H follows their ISB)")
     return ap.parse_args()
 
 
@@ -100,10 +103,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def workload_and_scheme(name):
+def workload_and_scheme(name, weights=None):
     from gbs_inputs import get_config
     from paper_1907_11771_b200 import scheme
     w = get_config(name)
+    if weights:
+        w = w.with_(weights=weights)
     counts, ws, _ = scheme.weight_set(w.weights, w.steps)
     wd = scheme.to_fp64(ws)
     H = scheme.macro_step(w.pde, w.order, w.n, counts, wd, w.h_factor)
@@ -153,7 +158,7 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    w, counts, wd, H = workload_and_scheme(a.config)
+    w, counts, wd, H = workload_and_scheme(a.config, a.weights)
     for _ in range(max(0, a.warmup)):
         time_oracle_sample(w, counts, wd, H, target=1e8)
     vals = []
@@ -190,7 +195,7 @@ def run_ours(a):
     dev = torch.device("cuda", local)
     if world > 1:
         pdist.init("nccl", dev)
-    w, counts, wd, H = workload_and_scheme(a.config)
+    w, counts, wd, H = workload_and_scheme(a.config, a.weights)
     # this rank's planes of the slowest axis (the whole grid on one GPU); every rank builds
     # only its slab of the seeded IC (bit-identical to the same planes of the full IC)
     plan = gbs.gbs_plan(w.pde, w.n, w.order, counts, world, rank, a.groups)
@@ -369,6 +374,7 @@ def run_ours(a):
                            "hbm_roofline_fraction_of_step": round(
                                value * 24 * F / (peak * 1e9 * world), 4)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "sim_time_per_s": H * a.steps / (ms * 1e-3),
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -163,6 +163,17 @@ def scheme(name: str, steps: Sequence[int] | None = None) -> Tuple[List[int], Li
         wmap = dict(zip(n_dep, c_dep))
         wmap.update(zip(n_free, c_free))
         return counts, [wmap[n] for n in counts], 8
+    if name == "opt8":
+        # input data: the Appendix-B optimised free weights (gbs_inputs/optimized_schemes.json);
+        # the dependent weights follow Eq. (6) here, by Gauss-Jordan
+        from gbs_inputs.schemes import optimized_for
+        if steps is None:
+            raise ValueError("opt8 needs the step counts")
+        s = optimized_for(steps)
+        c_free = [_F(x) for x in s["c_free"]]
+        c_dep = dependent_weights(s["n_dep"], s["n_free"], c_free, s["order"])
+        pairs = sorted(list(zip(s["n_dep"], c_dep)) + list(zip(s["n_free"], c_free)))
+        return [n for n, _ in pairs], [c for _, c in pairs], s["order"]
     raise KeyError(f"unknown weight set {name!r}")
 
 

@@ -113,6 +113,17 @@ def weight_set(name: str, steps: Sequence[int] | None = None) -> Tuple[List[int]
         w = dict(zip(nd, weights_exact(nd, nf, cf)))
         w.update(zip(nf, cf))
         return counts, [w[n] for n in counts], 8
+    if name == "opt8":
+        # Appendix-B optimised free weights for these step counts (gbs_inputs/
+        # optimized_schemes.json, written by tools/optimize_schemes.py); c_dep by Eq. (6)
+        from gbs_inputs.schemes import optimized_for
+        s = optimized_for(steps)
+        nd, nf = tuple(s["n_dep"]), tuple(s["n_free"])
+        cfree = [Fraction(x) for x in s["c_free"]]
+        w = dict(zip(nd, weights_exact(nd, nf, cfree)))
+        w.update(zip(nf, cfree))
+        counts = sorted(w)
+        return counts, [w[n] for n in counts], s["order"]
     raise KeyError(name)
 
 

@@ -202,6 +202,21 @@ def test_minimum_grid(torch_cuda, cfg, n, order):
     assert_parity(g[0], o[0], what=f"min grid {n}")
 
 
+@pytest.mark.parametrize("cfg,n,M", [("c4", (64, 32, 24), 3), ("c5", (64, 48, 40), 2),
+                                     ("c3", (192, 80, 1), 3), ("c2", (200, 136, 1), 4)])
+def test_optimised_weights_at_their_larger_step(torch_cuda, cfg, n, M):
+    """The Appendix-B optimised weights on the config's step counts ("opt8"), run at the H
+    their own ISB allows (2.1x / 3.1x the fallback's), through the default kernels
+    (two-substep 3-D, TMA 2-D, register 2-D for a ragged grid)."""
+    w = reduced(cfg, n, macro_steps=M, weights="opt8")
+    counts, wd, H = scheme_for(w)
+    c0, w0, H0 = scheme_for(reduced(cfg, n, macro_steps=M))
+    assert H > 2.0 * H0
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, M)
+    o = run_oracle(w, y0, counts, wd, H, M)
+    assert_parity(g[0], o[0], what=f"{cfg} opt8")
+
+
 def test_single_sequence_and_fd4_wave(torch_cuda):
     w = reduced("c4", (24, 20, 18), macro_steps=3).with_(order=4, steps=(2,))
     y0 = make_ic(w)
