@@ -209,10 +209,7 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *   "fuse"         1/0   two substeps per HBM pass on TMA grids (default 1)
  *   "persistent"   1/0   1-D grids up to 7000 points with m <= 16: every macro step of
  *                        a gbs_advance in one thread-block-cluster launch (default 1)
- *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)
- *   "l2hint"       0..3  two-substep kernel L2 eviction priorities: bit 0 = read-once
- *                        streams and all stores evict-first, bit 1 = stencil tiles
- *                        evict-last (default 0; measured within noise on C5)  */
+ *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)  */
 GBS_API int gbs_set_option(gbs_ctx* ctx, const char* key, int64_t value);
 
 /* Accumulated device time (ms) and launch count of the timed kernels of a class

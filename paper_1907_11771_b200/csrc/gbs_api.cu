@@ -164,7 +164,6 @@ struct gbs_ctx {
     int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
     int sms = 148;                    // streaming multiprocessors of the device
-    int l2hint = 0;                   // pair kernel L2 eviction hints (gbs_wave3d_pair.cuh)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     double graph_H = -1.0;
     int64_t macro_done = 0;
@@ -602,7 +601,6 @@ static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
     a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
     a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
     a.nonfinite = op.flag ? c->d_flag : nullptr;
-    a.l2hint = c->l2hint;
     a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, s.nz) : (int)std::min<int64_t>(128, s.nz);
     dim3 grid((unsigned)(c->n[0] / gbs::tma::TX), (unsigned)(c->n[1] / gbs::tma::TY),
               (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
@@ -1139,7 +1137,6 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     };
     if (k == "graph") { c->use_graph = value != 0 && c->world == 1; drop_graphs(); return GBS_OK; }
     if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
-    if (k == "l2hint") { c->l2hint = (int)value; drop_graphs(); return GBS_OK; }
     if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }

@@ -77,8 +77,6 @@ struct PairArgs {
     double sx2, sy2, sz2;
     double cfA, cfB, wh;
     int* nonfinite;
-    int l2hint;                       // bit 0: read-once streams and stores evict-first in L2;
-                                      // bit 1: S_u / U tiles and centres evict-last
 };
 
 template <int R, int MODEB, bool SLAB>
@@ -114,12 +112,12 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
 
     auto load_tile = [&](double* dst, const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int z,
-                         uint64_t* bar, uint64_t pol) {
-        tma_load_3d_hint(dst, b, x0, ytop, z, bar, pol);
-        tma_load_3d_hint(dst + R * TX, a, x0, y0, z, bar, pol);
-        tma_load_3d_hint(dst + (R + TY) * TX, b, x0, ybot, z, bar, pol);
-        tma_load_3d_hint(dst + L::CENTER, c, xl, y0, z, bar, pol);
-        tma_load_3d_hint(dst + L::CENTER + L::STRIP, c, xr, y0, z, bar, pol);
+                         uint64_t* bar) {
+        tma_load_3d(dst, b, x0, ytop, z, bar);
+        tma_load_3d(dst + R * TX, a, x0, y0, z, bar);
+        tma_load_3d(dst + (R + TY) * TX, b, x0, ybot, z, bar);
+        tma_load_3d(dst + L::CENTER, c, xl, y0, z, bar);
+        tma_load_3d(dst + L::CENTER + L::STRIP, c, xr, y0, z, bar);
     };
     auto issue_stage = [&](int i) {
         const int s = i % D;
@@ -127,17 +125,15 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         mbar_expect_tx(&full[s], L::stage_bytes);
         double* st = stages + (size_t)s * STAGE;
         const int z = zc(z0 + i), zf = zc(z0 + i + R);
-        const uint64_t keep = (A.l2hint & 2) ? policy_evict_last() : policy_evict_normal();
-        const uint64_t once = (A.l2hint & 1) ? policy_evict_first() : policy_evict_normal();
-        load_tile(st, &M.su_a, &M.su_b, &M.su_c, z, &full[s], keep);
-        load_tile(st + L::O_UT, &M.u_a, &M.u_b, &M.u_c, z, &full[s], keep);
-        tma_load_3d_hint(st + L::O_SUF, &M.su_a, x0, y0, zf, &full[s], keep);
-        tma_load_3d_hint(st + L::O_UF, &M.u_a, x0, y0, zf, &full[s], keep);
-        tma_load_3d_hint(st + L::O_SV, &M.sv, x0, y0, z, &full[s], once);
-        tma_load_3d_hint(st + L::O_PV, &M.pv, x0, y0, z, &full[s], once);
+        load_tile(st, &M.su_a, &M.su_b, &M.su_c, z, &full[s]);
+        load_tile(st + L::O_UT, &M.u_a, &M.u_b, &M.u_c, z, &full[s]);
+        tma_load_3d(st + L::O_SUF, &M.su_a, x0, y0, zf, &full[s]);
+        tma_load_3d(st + L::O_UF, &M.u_a, x0, y0, zf, &full[s]);
+        tma_load_3d(st + L::O_SV, &M.sv, x0, y0, z, &full[s]);
+        tma_load_3d(st + L::O_PV, &M.pv, x0, y0, z, &full[s]);
         if constexpr (MODEB == MODE_FINACC) {
-            tma_load_3d_hint(st + L::O_AC, &M.acc_u, x0, y0, z, &full[s], once);
-            tma_load_3d_hint(st + L::O_AC + L::PWT, &M.acc_v, x0, y0, z, &full[s], once);
+            tma_load_3d(st + L::O_AC, &M.acc_u, x0, y0, z, &full[s]);
+            tma_load_3d(st + L::O_AC + L::PWT, &M.acc_v, x0, y0, z, &full[s]);
         }
     };
 
@@ -266,16 +262,15 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
             else bad |= !isfinite(ub[p]) || !isfinite(vb[p]);
         }
         const int64_t oz = zoff(z0 + i);
-        const uint64_t wpol = (A.l2hint & 1) ? policy_evict_first() : policy_evict_normal();
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int64_t o = oz + own + (int64_t)r * nx;
             if constexpr (MODEB == MODE_LF) {
-                st_stream(A.Av + o, va[2 * r], va[2 * r + 1], wpol);
-                st_stream(A.Cu + o, uc[2 * r], uc[2 * r + 1], wpol);
+                *reinterpret_cast<double2*>(A.Av + o) = make_double2(va[2 * r], va[2 * r + 1]);
+                *reinterpret_cast<double2*>(A.Cu + o) = make_double2(uc[2 * r], uc[2 * r + 1]);
             }
-            st_stream(A.Bu + o, ub[2 * r], ub[2 * r + 1], wpol);
-            st_stream(A.Bv + o, vb[2 * r], vb[2 * r + 1], wpol);
+            *reinterpret_cast<double2*>(A.Bu + o) = make_double2(ub[2 * r], ub[2 * r + 1]);
+            *reinterpret_cast<double2*>(A.Bv + o) = make_double2(vb[2 * r], vb[2 * r + 1]);
         }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j)
