@@ -118,7 +118,8 @@ def workload_and_scheme(name, weights=None):
 def describe(w, H):
     pde = {"adv1d": "1-D advection", "acoustic2d": "2-D acoustics", "wave3d": "3-D scalar wave"}[w.pde]
     grid = "x".join(str(v) for v in w.n[: w.ndim])
-    return (f"{w.name}: {pde} {grid}, FD{w.order}, step counts {{{','.join(map(str, w.steps))}}} "
+    disc = "spectral" if w.order == 0 else f"FD{w.order}"
+    return (f"{w.name}: {pde} {grid}, {disc}, step counts {{{','.join(map(str, w.steps))}}} "
             f"({w.weights} weights), H={H:.6g}, seeded {w.ic} IC")
 
 
@@ -150,7 +151,8 @@ def time_oracle_sample(w, counts, wd, H, target=1.0e9):
     units = ws.points * S * macro
     grid = "x".join(str(v) for v in n[: w.ndim])
     return {"value": units / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{macro} macro step(s) of the {w.name} scheme (same PDE, FD{w.order}, steps, "
+            "sample": f"{macro} macro step(s) of the {w.name} scheme (same PDE, "
+                      f"{'spectral' if w.order == 0 else 'FD%d' % w.order}, steps, "
                       f"weights, H) on a {grid} grid = {units:.3g} pt-substeps in {dt:.2f} s"}
 
 

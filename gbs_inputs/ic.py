@@ -153,6 +153,9 @@ def make_ic(w: Workload, srange=None) -> np.ndarray:
         raise ValueError("1-D states are not slabbed")
     if w.ic == "gauss1d":
         y = gauss1d(nx, w.seed)
+    elif w.ic == "cos1d":
+        # PAPER.md §4.1 (line 560): u(x, 0) = (1 - cos 2 pi x) / 2 on [0, 1) (no random draw)
+        y = (0.5 * (1.0 - np.cos(2.0 * np.pi * np.arange(nx) / nx)))[None, :]
     elif w.ic == "gauss2d_sum8":
         y = gauss2d_sum8(nx, ny, w.seed)
         if srange is not None:

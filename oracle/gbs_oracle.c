@@ -32,7 +32,13 @@
  *   ADV1D      u_t = -u_x
  *   ACOUSTIC2D p_t = -(u_x + v_y), u_t = -p_x, v_t = -p_y
  *   WAVE3D     u_t = v, v_t = u_xx + u_yy + u_zz
- * with centered periodic FD derivatives in the antisymmetric pairing form
+ * ADV1D with order 0 is the paper's own spectral derivative (PAPER.md:565,
+ * §4.1): the derivative of the trigonometric interpolant, by its definition
+ * -- a forward DFT, multiplication by 2 pi i k for |k| < N/2 (the Nyquist
+ * mode of an even-N grid has no odd derivative and is dropped), an inverse
+ * DFT -- as plain O(N^2) loops over a cos/sin table of 2 pi m / N.
+ * Otherwise the derivatives are
+ * centered periodic FD derivatives in the antisymmetric pairing form
  * (SURVEY.md §8(c) item 3), grid spacing 1/N_d on the unit box (S6):
  *   D1 u_i = N_d * sum_{j=1..r} a_j (u_{i+j} - u_{i-j})
  *   D2 u_i = N_d^2 * (b_0 u_i + sum_{j=1..r} b_j (u_{i+j} + u_{i-j}))
@@ -51,6 +57,10 @@
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
+#endif
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
 #endif
 
 #define ORACLE_ADV1D 1
@@ -105,7 +115,14 @@ typedef struct {
     const double* a;            /* D1 coefficients */
     const double* b;            /* D2 coefficients */
     double b0;
+    double *ct, *st;            /* spectral (order 0): cos, sin of 2 pi m / nx */
+    double *re, *im;            /* spectral scratch: DFT of the field */
 } grid_t;
+
+static void release(grid_t* g) {
+    free(g->ct); free(g->st); free(g->re); free(g->im);
+    g->ct = g->st = g->re = g->im = NULL;
+}
 
 static int setup(grid_t* g, int pde, int order, const int64_t* dims, const double* scale) {
     memset(g, 0, sizeof(*g));
@@ -113,6 +130,19 @@ static int setup(grid_t* g, int pde, int order, const int64_t* dims, const doubl
     g->order = order;
     if (order == 4) { g->r = 2; g->a = A4; g->b = B4; g->b0 = B4_0; }
     else if (order == 8) { g->r = 4; g->a = A8; g->b = B8; g->b0 = B8_0; }
+    else if (order == 0 && pde == ORACLE_ADV1D && dims[0] >= 2 && dims[0] % 2 == 0) {
+        int64_t m, n = dims[0];
+        g->r = 0;
+        g->ct = (double*)malloc(sizeof(double) * (size_t)n);
+        g->st = (double*)malloc(sizeof(double) * (size_t)n);
+        g->re = (double*)malloc(sizeof(double) * (size_t)n);
+        g->im = (double*)malloc(sizeof(double) * (size_t)n);
+        if (!g->ct || !g->st || !g->re || !g->im) { release(g); return -7; }
+        for (m = 0; m < n; ++m) {
+            g->ct[m] = cos(2.0 * M_PI * (double)m / (double)n);
+            g->st[m] = sin(2.0 * M_PI * (double)m / (double)n);
+        }
+    }
     else return -1;
     g->nx = dims[0]; g->ny = dims[1]; g->nz = dims[2];
     g->sx = scale[0]; g->sy = scale[1]; g->sz = scale[2];
@@ -174,11 +204,48 @@ static double d2z(const grid_t* g, const double* u, int64_t x, int64_t y, int64_
     return g->sz * g->sz * s;
 }
 
+/* spectral u_x on the unit periodic interval (order 0): u_hat_k = sum_j u_j
+ * e^{-2 pi i j k / N}; u_x(j) = (1/N) sum_{|k| < N/2} 2 pi i k u_hat_k e^{2 pi i j k / N}
+ * (k and N - k taken together: the result is real) */
+static void spectral_d1(const grid_t* g, const double* u, double* du) {
+    const int64_t n = g->nx;
+    int64_t k, j;
+#pragma omp parallel for num_threads(g_threads) schedule(static)
+    for (k = 0; k < n; ++k) {
+        double re = 0.0, im = 0.0;
+        int64_t jj;
+        for (jj = 0; jj < n; ++jj) {
+            int64_t m = (jj * k) % n;
+            re += u[jj] * g->ct[m];
+            im -= u[jj] * g->st[m];
+        }
+        g->re[k] = re;
+        g->im[k] = im;
+    }
+#pragma omp parallel for num_threads(g_threads) schedule(static)
+    for (j = 0; j < n; ++j) {
+        double s = 0.0;
+        int64_t kk;
+        for (kk = 1; kk < n / 2; ++kk) {
+            /* mode kk and its conjugate -kk: 2 Re(2 pi i kk u_hat_kk e^{2 pi i j kk / N}) */
+            int64_t m = (j * kk) % n;
+            double wre = -2.0 * M_PI * (double)kk * g->im[kk];   /* Re(2 pi i kk u_hat) */
+            double wim = 2.0 * M_PI * (double)kk * g->re[kk];    /* Im(2 pi i kk u_hat) */
+            s += 2.0 * (wre * g->ct[m] - wim * g->st[m]);
+        }
+        du[j] = s / (double)n;
+    }
+}
+
 /* f = rhs(y): the MOL right-hand side, SoA [F][nz][ny][nx] */
 static void rhs(const grid_t* g, const double* y, double* f) {
     int64_t n = g->npts;
     int64_t z;
-    if (g->pde == ORACLE_ADV1D) {
+    if (g->pde == ORACLE_ADV1D && g->order == 0) {
+        int64_t x;
+        spectral_d1(g, y, f);
+        for (x = 0; x < g->nx; ++x) f[x] = -f[x];
+    } else if (g->pde == ORACLE_ADV1D) {
         const double* u = y;
         int64_t x;
 #pragma omp parallel for num_threads(g_threads) schedule(static)
@@ -224,6 +291,7 @@ int oracle_rhs(int pde, int order, const int64_t* dims, const double* scale,
     int rc = setup(&g, pde, order, dims, scale);
     if (rc) return rc;
     rhs(&g, y, f);
+    release(&g);
     return 0;
 }
 
@@ -241,10 +309,10 @@ int oracle_advance(int pde, int order, const int64_t* dims, const double* scale,
     int k;
     double *bufs[4], *f, *acc;
     if (rc) return rc;
-    if (m < 1) return -4;
+    if (m < 1) { release(&g); return -4; }
     for (k = 0; k < m; ++k)
-        if (n_k[k] < 2 || (n_k[k] % 2) != 0) return -5;
-    if (!(H > 0.0)) return -6;
+        if (n_k[k] < 2 || (n_k[k] % 2) != 0) { release(&g); return -5; }
+    if (!(H > 0.0)) { release(&g); return -6; }
     len = g.F * g.npts;
     for (k = 0; k < 4; ++k) {
         bufs[k] = (double*)malloc(sizeof(double) * (size_t)len);
@@ -286,6 +354,7 @@ int oracle_advance(int pde, int order, const int64_t* dims, const double* scale,
     for (k = 0; k < 4; ++k) free(bufs[k]);
     free(f);
     free(acc);
+    release(&g);
     return 0;
 }
 
@@ -303,6 +372,7 @@ int oracle_component(int pde, int order, const int64_t* dims, const double* scal
     int rc = setup(&g, pde, order, dims, scale);
     if (rc) return rc;
     len = g.F * g.npts;
+    release(&g);
     memcpy(out, Y, sizeof(double) * (size_t)len);
     return oracle_advance(pde, order, dims, scale, 1, &nk, &w, H, 1, out);
 }

@@ -179,6 +179,10 @@ def _max_on_circle(fun, tol: float = 1e-15) -> float:
 def rho(pde: str, order: int, n: Sequence[int]) -> float:
     """max |lambda| over the continuous-theta symbol of the config's operator."""
     nx, ny, nz = n
+    if pde == "adv1d" and order == 0:
+        # spectral derivative: lambda = Delta t / Delta x = 0.99/pi ISB, "the factor of pi
+        # arises from the spectral spatial derivatives" (PAPER.md:566-568): rho = pi / Delta x
+        return float(np.pi * nx)
     if pde == "adv1d":
         kmax = _max_on_circle(lambda t: np.abs(fd.d1_symbol(order, t)))
         return nx * kmax

@@ -117,6 +117,9 @@ static bool make_map(CUtensorMap* m, double* base, int64_t nx, int64_t ny, int64
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static constexpr int kClusterMaxN = 7000;     // 4 nx doubles of shared memory per CTA
+static constexpr int kSpectralMaxN = 6400;    // 4.5 nx doubles (state, levels, weights)
+
 struct KernelTimer {
     std::vector<cudaEvent_t> ev;      // pairs
     std::vector<int> cls;
@@ -156,6 +159,7 @@ struct gbs_ctx {
     bool time_kernels = false;
     bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
     bool use_persistent = true;       // one cluster launch per gbs_advance for small 1-D grids
+    double* d_alpha = nullptr;        // spectral derivative weights (order 0)
     int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
     double* d_wh = nullptr;
     bool use_fuse = true;             // two-substep (temporally blocked) kernels where eligible
@@ -846,7 +850,6 @@ static int enqueue_macro(gbs_ctx* c, double H) {
 // ---------------------------------------------------------------------------
 // small 1-D grids: the whole run in one cluster launch (K6)
 // ---------------------------------------------------------------------------
-static constexpr int kClusterMaxN = 7000;     // 4 nx doubles of shared memory per CTA
 
 static bool persistent_path(const gbs_ctx* c) {
     const int m = (int)c->my_seq.size();
@@ -874,7 +877,43 @@ static int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H) {
     a.nk = c->d_nk;
     a.wh = c->d_wh;
     a.nonfinite = c->d_flag;
-    const size_t smem = sizeof(double) * 4 * (size_t)a.nx;
+    const bool spectral = c->order == 0;
+    const size_t smem = sizeof(double) * (4 * (size_t)a.nx + (spectral ? (size_t)a.nx / 2 : 0));
+    if (spectral && !c->d_alpha) {
+        // alpha_j = pi (-1)^{j+1} cot(j pi / N) / N, j = 1 .. N/2 - 1 (gbs_adv1d_cluster.cuh)
+        const int64_t N = c->n[0];
+        std::vector<double> al((size_t)(N / 2 - 1));
+        for (int64_t j = 1; j <= N / 2 - 1; ++j)
+            al[(size_t)(j - 1)] = (j % 2 ? 1.0 : -1.0) * M_PI / std::tan((double)j * M_PI / (double)N) / (double)N;
+        CU(c, cudaMalloc(&c->d_alpha, sizeof(double) * al.size() + 8));
+        CU(c, cudaMemcpyAsync(c->d_alpha, al.data(), sizeof(double) * al.size(), cudaMemcpyHostToDevice,
+                              c->stream));
+    }
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (spectral) {
+        auto kern = gbs::adv1d_cluster_run_spectral;
+        CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (m > 8) CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)m);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)m;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const double* alpha = c->d_alpha;
+        if (c->time_kernels && (rc = timed_begin(c, 5, &end))) return rc;
+        CU(c, cudaLaunchKernelEx(&cfg, kern, a, alpha));
+        if (end) CU(c, cudaEventRecord(end, c->stream));
+        c->launches++;
+        return GBS_OK;
+    }
     void (*kern)(const gbs::Adv1DClusterArgs) =
         c->R == 2 ? gbs::adv1d_cluster_run<2> : gbs::adv1d_cluster_run<4>;
     CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -891,8 +930,6 @@ static int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    int rc;
-    cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, 5, &end))) return rc;
     CU(c, cudaLaunchKernelEx(&cfg, kern, a));
     if (end) CU(c, cudaEventRecord(end, c->stream));
@@ -953,6 +990,7 @@ void gbs_destroy(gbs_ctx* c) {
     if (c->d_gather) cudaFree(c->d_gather);
     if (c->d_nk) cudaFree(c->d_nk);
     if (c->d_wh) cudaFree(c->d_wh);
+    if (c->d_alpha) cudaFree(c->d_alpha);
     for (auto e : c->timer.ev) cudaEventDestroy(e);
     auto& A = nccl::api();
     if (A.ok) {
@@ -975,8 +1013,18 @@ static int validate(gbs_ctx* c, const gbs_grid* g, int stencil_order, int m, con
     else if (g->pde == GBS_WAVE3D) { c->ndim = 3; c->F = 2; }
     else return fail(c, GBS_E_INVAL, "grid.pde=%d is not a known PDE", g->pde);
     if (g->ndim != c->ndim) return fail(c, GBS_E_INVAL, "grid.ndim=%d does not match the PDE", g->ndim);
-    if (stencil_order != 4 && stencil_order != 8)
-        return fail(c, GBS_E_INVAL, "stencil_order=%d (must be 4 or 8)", stencil_order);
+    if (stencil_order == 0) {
+        // spectral derivative: 1-D advection on an even grid, whole run in
+        // the cluster kernel (N <= kClusterMaxN, m <= 16, one GPU)
+        if (g->pde != GBS_ADV1D)
+            return fail(c, GBS_E_INVAL, "stencil_order=0 (spectral) is defined for GBS_ADV1D only");
+        if (g->n[0] < 4 || g->n[0] % 2 || g->n[0] > kSpectralMaxN)
+            return fail(c, GBS_E_INVAL, "spectral grid n[0]=%lld must be even, 4..%d", (long long)g->n[0],
+                        kSpectralMaxN);
+        if (m > 16) return fail(c, GBS_E_INVAL, "spectral runs one sequence per CTA of a cluster: m=%d > 16", m);
+    } else if (stencil_order != 4 && stencil_order != 8) {
+        return fail(c, GBS_E_INVAL, "stencil_order=%d (must be 4 or 8, or 0 = spectral)", stencil_order);
+    }
     c->order = stencil_order;
     c->R = stencil_order / 2;
     for (int d = 0; d < 3; ++d) {
@@ -1186,6 +1234,9 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
         c->t += H * (double)macro_steps;
         return GBS_OK;
     }
+    if (c->order == 0)
+        return fail(c, GBS_E_UNSUPPORTED, "the spectral derivative runs only in the cluster kernel "
+                                          "(one GPU, no loopback, option persistent=1)");
     const bool graph = c->use_graph && !c->time_kernels && macro_steps > 0;
     if (graph && c->graph_H != H) {
         for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }

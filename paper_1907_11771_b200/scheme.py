@@ -194,6 +194,8 @@ def _d2_symbol_max(order: int) -> float:
 
 def spectral_radius(pde: str, order: int, n: Sequence[int], length=(1.0, 1.0, 1.0)) -> float:
     s = [n[d] / length[d] for d in range(3)]
+    if pde == "adv1d" and order == 0:
+        return math.pi * s[0]               # spectral: pi / dx
     if pde == "adv1d":
         return s[0] * _d1_symbol_max(order)
     if pde == "acoustic2d":

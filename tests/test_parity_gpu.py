@@ -217,6 +217,36 @@ def test_optimised_weights_at_their_larger_step(torch_cuda, cfg, n, M):
     assert_parity(g[0], o[0], what=f"{cfg} opt8")
 
 
+@pytest.mark.parametrize("wset,N", [("GBS_8_6", 64), ("GBS_12_8", 64), ("GBS_8_6", 256),
+                                    ("GBS_12_8", 128), ("square8", 50), ("GBS_8_8", 32)])
+def test_spectral_section41(torch_cuda, wset, N):
+    """The paper's own experiment (§4.1): spectral derivative (order 0, circulant
+    pairing form in the cluster kernel), IC (1 - cos 2 pi x)/2, lambda = 0.99/pi ISB, one
+    period.  Against the oracle (DFT derivative) and the exact solution."""
+    import math
+    w = get_config("s41").with_(n=(N, 1, 1))
+    counts, ws, _ = W.scheme(wset)
+    wd = W.to_double(ws)
+    M = math.ceil(1.0 / S.macro_step_H("adv1d", 0, w.n, counts, wd, w.h_factor))
+    w = w.with_(steps=tuple(counts), weights=wset, macro_steps=M)
+    y0, g, info = run_gpu(torch_cuda, w, counts, wd, 1.0 / M, M)
+    o = run_oracle(w, y0, counts, wd, 1.0 / M, M)
+    assert info["kernel_launches"] == 1
+    assert_parity(g[0], o[0], what=f"s41 {wset} N={N}")
+    err_gpu = np.max(np.abs(g[0] - y0))
+    err_or = np.max(np.abs(o[0] - y0))
+    assert err_gpu <= 1.01 * err_or + 1e-13
+
+
+def test_spectral_is_cluster_only(torch_cuda):
+    gbs = gbs_mod()
+    with gbs.Stepper("adv1d", (64, 1, 1), 0, [2, 4], [-1 / 3, 4 / 3], persistent=0) as st:
+        st.write(np.ones((1, 64)))
+        with pytest.raises(gbs.GbsError) as e:
+            st.advance(1, 1e-3)
+        assert e.value.code == gbs.GBS_E_UNSUPPORTED
+
+
 def test_single_sequence_and_fd4_wave(torch_cuda):
     w = reduced("c4", (24, 20, 18), macro_steps=3).with_(order=4, steps=(2,))
     y0 = make_ic(w)
