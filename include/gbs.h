@@ -14,8 +14,8 @@
  * and the new state is  Y <- sum_k w_k y*_k,  summed in ascending n_k order.
  * f is the method-of-lines right-hand side of a built-in linear PDE on a
  * periodic box with centered finite differences of order 4 or 8
- * (BASELINE.json configs; the paper itself uses a spectral derivative,
- * see DESIGN.md):
+ * (BASELINE.json configs) or, for GBS_ADV1D, the paper's own spectral
+ * (Fourier collocation) derivative (stencil_order 0; §4.1):
  *
  *     GBS_ADV1D       u_t = -u_x                                   F = 1
  *     GBS_ACOUSTIC2D  p_t = -(u_x + v_y), u_t = -p_x, v_t = -p_y    F = 3
@@ -152,7 +152,10 @@ GBS_API int gbs_halo_schedule(int slabs, int my_slab, int64_t nz_local, int ghos
 
 /* Create a context: validate, plan, allocate, and (multi-GPU) join NCCL.
  *   grid           problem description (copied)
- *   stencil_order  4 or 8 (centered FD, radius r = order / 2)
+ *   stencil_order  4 or 8 (centered FD, radius r = order / 2), or 0: spectral
+ *                  derivative of the trigonometric interpolant (GBS_ADV1D only,
+ *                  n[0] even, 4..6400, m <= 16; runs as one thread-block-cluster
+ *                  launch per gbs_advance on one GPU -- GBS_E_UNSUPPORTED otherwise)
  *   m, n_k, w_k    step counts (even, >= 2, distinct; 1 <= m <= 32) and their
  *                  fp64 weights (already rounded once from exact rationals by
  *                  the caller); both copied.  Sequences with
