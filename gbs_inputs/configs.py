@@ -82,10 +82,13 @@ CONFIGS = {
     "c5": Workload("c5", "wave3d", (1024, 1024, 1024), 8,
                    (2, 4, 6, 8, 10, 12, 14, 16), "fallback8", 4,
                    "bandlimited3d", 1005),
-    # The paper's own experiment (§4.1), not a
-    # BASELINE.json config: one-way wave u_t + u_x = 0 on [0,1), spectral derivative (order 0),
+}
+
+# The paper's own experiment (§4.1), not a
+# BASELINE.json config: one-way wave u_t + u_x = 0 on [0,1), spectral derivative (order 0),
     # IC (1 - cos 2 pi x)/2, GBS_8,6, lambda = dt/dx = 0.99/pi ISB (h_factor 0.99 with
     # rho = pi N), one period (macro steps = ceil(1 / H_max), H = 1 / macro steps).
+PAPER_WORKLOADS = {
     "s41": Workload("s41", "adv1d", (64, 1, 1), 0, tuple(range(2, 23, 2)), "GBS_8_6", 0,
                     "cos1d", 0, h_factor=0.99,
                     notes="PAPER.md 4.1 one-way wave, spectral, one period"),
@@ -93,10 +96,12 @@ CONFIGS = {
 
 
 def get_config(name: str) -> Workload:
-    try:
-        return CONFIGS[name.lower()]
-    except KeyError as e:
-        raise KeyError(f"unknown config {name!r}; known: {sorted(CONFIGS)}") from e
+    key = name.lower()
+    if key in CONFIGS:
+        return CONFIGS[key]
+    if key in PAPER_WORKLOADS:
+        return PAPER_WORKLOADS[key]
+    raise KeyError(f"unknown config {name!r}; known: {sorted(CONFIGS) + sorted(PAPER_WORKLOADS)}")
 
 
 def reduced(name: str, n: Tuple[int, int, int], macro_steps: int | None = None,
