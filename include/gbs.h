@@ -189,7 +189,22 @@ GBS_API int gbs_read_state(gbs_ctx* ctx, double* dst, int64_t count, int on_devi
 GBS_API int gbs_write_slab(gbs_ctx* ctx, const double* src, int64_t count, int on_device);
 GBS_API int gbs_read_slab(gbs_ctx* ctx, double* dst, int64_t count, int on_device);
 
-/* Wait for all queued work; surfaces deferred errors. */
+/* Asynchronous slab IO (same layout and count as gbs_write_slab / gbs_read_slab; on one
+ * GPU the slab is the whole grid).  The copies run on the context's own copy streams and
+ * overlap the macro steps queued on the context stream:
+ *   gbs_write_slab_async  stages src (pinned host or device) into a staging buffer; the
+ *                         staged state becomes Y before the next gbs_advance / read / sync.
+ *                         src must stay valid and unmodified until the next gbs_sync.
+ *   gbs_read_slab_async   snapshots the current Y (after every macro step queued so far)
+ *                         and copies it to dst; dst is complete after the next gbs_sync,
+ *                         which also surfaces deferred errors.
+ * Staging costs 2 x F x slab points x 8 bytes of device memory, allocated on first use.
+ * A write-advance-read loop with these calls keeps the host<->device copies of one step
+ * under the macro steps of the neighbouring ones. */
+GBS_API int gbs_write_slab_async(gbs_ctx* ctx, const double* src, int64_t count, int on_device);
+GBS_API int gbs_read_slab_async(gbs_ctx* ctx, double* dst, int64_t count, int on_device);
+
+/* Wait for all queued work (compute and asynchronous copies); surfaces deferred errors. */
 GBS_API int gbs_sync(gbs_ctx* ctx);
 
 /* Release everything the context owns (NULL is a no-op). */

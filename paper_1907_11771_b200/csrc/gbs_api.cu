@@ -160,6 +160,12 @@ struct gbs_ctx {
     bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
     bool use_persistent = true;       // one cluster launch per gbs_advance for small 1-D grids
     double* d_alpha = nullptr;        // spectral derivative weights (order 0)
+    // asynchronous slab IO (gbs_write_slab_async / gbs_read_slab_async): per local slab a
+    // staging buffer for the incoming and for the outgoing state, own copy streams
+    std::vector<double*> in_buf, out_buf;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr, ev_out_ready = nullptr, ev_out_free = nullptr;
+    bool pending_in = false;
     int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
     double* d_wh = nullptr;
     bool use_fuse = true;             // two-substep (temporally blocked) kernels where eligible
@@ -937,6 +943,64 @@ static int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H) {
     return GBS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// asynchronous slab IO: the copies run on their own streams and overlap the
+// macro steps of the context stream; the state moves between the staging
+// buffers and Y by device-to-device copies on the context stream, ordered by
+// events (IN: h2d -> ready -> D2D into Y -> free; OUT: D2D from Y -> ready ->
+// d2h -> free).
+// ---------------------------------------------------------------------------
+static int async_setup(gbs_ctx* c) {
+    if (!c->in_buf.empty()) return GBS_OK;
+    if (!c->h2d) {
+        CU(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        CU(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&c->ev_in_ready, &c->ev_in_free, &c->ev_out_ready, &c->ev_out_free})
+            CU(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    for (auto& s : c->slab) {
+        const size_t bytes = sizeof(double) * (size_t)c->F * (size_t)(s.nz * c->plane);
+        double *in = nullptr, *out = nullptr;
+        if (cudaMalloc(&in, bytes) != cudaSuccess || cudaMalloc(&out, bytes) != cudaSuccess) {
+            if (in) cudaFree(in);
+            return fail(c, GBS_E_NOMEM, "cudaMalloc of 2 x %zu bytes (async IO staging) failed", bytes);
+        }
+        c->in_buf.push_back(in);
+        c->out_buf.push_back(out);
+    }
+    // nothing is in flight yet: both staging buffers start free
+    CU(c, cudaEventRecord(c->ev_in_free, c->stream));
+    CU(c, cudaEventRecord(c->ev_out_free, c->stream));
+    return GBS_OK;
+}
+
+// drop the staging buffers (their sizes follow the slab layout); streams and events stay
+static void async_release(gbs_ctx* c) {
+    if (c->h2d) cudaStreamSynchronize(c->h2d);
+    if (c->d2h) cudaStreamSynchronize(c->d2h);
+    for (double* p : c->in_buf) cudaFree(p);
+    for (double* p : c->out_buf) cudaFree(p);
+    c->in_buf.clear();
+    c->out_buf.clear();
+    c->pending_in = false;
+}
+
+// a staged incoming state becomes Y (in context-stream order)
+static int consume_in(gbs_ctx* c) {
+    if (!c->pending_in) return GBS_OK;
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_in_ready, 0));
+    for (size_t v = 0; v < c->slab.size(); ++v) {
+        Slab& s = c->slab[v];
+        const int64_t n = s.nz * c->plane;
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(field_ptr(c, s, c->yb, f), c->in_buf[v] + (int64_t)f * n,
+                                  sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CU(c, cudaEventRecord(c->ev_in_free, c->stream));
+    c->pending_in = false;
+    return GBS_OK;
+}
+
 static int check_flag(gbs_ctx* c) {
     int h = 0;
     CU(c, cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -984,6 +1048,14 @@ int gbs_nccl_unique_id(void* out128) {
 void gbs_destroy(gbs_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->h2d) { cudaStreamSynchronize(c->h2d); cudaStreamDestroy(c->h2d); }
+    if (c->d2h) { cudaStreamSynchronize(c->d2h); cudaStreamDestroy(c->d2h); }
+    for (cudaEvent_t e : {c->ev_in_ready, c->ev_in_free, c->ev_out_ready, c->ev_out_free})
+        if (e) cudaEventDestroy(e);
+    for (double* p : c->in_buf) cudaFree(p);
+    for (double* p : c->out_buf) cudaFree(p);
+    c->in_buf.clear();
+    c->out_buf.clear();
     for (auto& g : c->gexec) if (g) cudaGraphExecDestroy(g);
     free_state(c);
     if (c->d_flag) cudaFree(c->d_flag);
@@ -1198,6 +1270,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
                         (long long)value, (long long)c->nslow);
         cudaStreamSynchronize(c->stream);
         drop_graphs();
+        async_release(c);
         free_state(c);
         if (c->d_flag) { cudaFree(c->d_flag); c->d_flag = nullptr; }
         c->loopback = (int)value;
@@ -1212,6 +1285,8 @@ int gbs_write_state(gbs_ctx* c, const double* src, int64_t count, int on_device)
     if (count != c->F * c->points)
         return fail(c, GBS_E_INVAL, "count=%lld, expected F*points=%lld", (long long)count, (long long)(c->F * c->points));
     CU(c, cudaSetDevice(c->device));
+    int rc0 = consume_in(c);
+    if (rc0) return rc0;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     for (auto& s : c->slab)
         for (int f = 0; f < c->F; ++f)
@@ -1228,6 +1303,7 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
     if (!(H > 0.0) || !std::isfinite(H)) return fail(c, GBS_E_INVAL, "H=%g must be positive and finite", H);
     CU(c, cudaSetDevice(c->device));
     int rc;
+    if ((rc = consume_in(c))) return rc;
     if (macro_steps > 0 && persistent_path(c)) {
         if ((rc = launch_cluster_run(c, macro_steps, H))) return rc;
         c->macro_done += macro_steps;
@@ -1273,7 +1349,11 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
 int gbs_sync(gbs_ctx* c) {
     if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
     CU(c, cudaSetDevice(c->device));
+    int rc = consume_in(c);
+    if (rc) return rc;
     CU(c, cudaStreamSynchronize(c->stream));
+    if (c->h2d) CU(c, cudaStreamSynchronize(c->h2d));
+    if (c->d2h) CU(c, cudaStreamSynchronize(c->d2h));
     return check_flag(c);
 }
 
@@ -1283,6 +1363,8 @@ int gbs_read_state(gbs_ctx* c, double* dst, int64_t count, int on_device) {
     if (count != c->F * c->points)
         return fail(c, GBS_E_INVAL, "count=%lld, expected F*points=%lld", (long long)count, (long long)(c->F * c->points));
     CU(c, cudaSetDevice(c->device));
+    int rc0 = consume_in(c);
+    if (rc0) return rc0;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     if (c->slabs == 1) {
         for (auto& s : c->slab)
@@ -1322,6 +1404,8 @@ int gbs_write_slab(gbs_ctx* c, const double* src, int64_t count, int on_device) 
         return fail(c, GBS_E_INVAL, "count=%lld, expected F*slab points=%lld", (long long)count,
                     (long long)(c->F * per_field));
     CU(c, cudaSetDevice(c->device));
+    int rc0 = consume_in(c);
+    if (rc0) return rc0;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     for (auto& s : c->slab)
         for (int f = 0; f < c->F; ++f)
@@ -1341,6 +1425,8 @@ int gbs_read_slab(gbs_ctx* c, double* dst, int64_t count, int on_device) {
         return fail(c, GBS_E_INVAL, "count=%lld, expected F*slab points=%lld", (long long)count,
                     (long long)(c->F * per_field));
     CU(c, cudaSetDevice(c->device));
+    int rc0 = consume_in(c);
+    if (rc0) return rc0;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     for (auto& s : c->slab)
         for (int f = 0; f < c->F; ++f)
@@ -1349,6 +1435,69 @@ int gbs_read_slab(gbs_ctx* c, double* dst, int64_t count, int on_device) {
     int rc = gbs_sync(c);
     if (rc) return rc;
     return harvest_timer(c);
+}
+
+int gbs_write_slab_async(gbs_ctx* c, const double* src, int64_t count, int on_device) {
+    if (!c || !src) return fail(c, GBS_E_INVAL, "ctx or src is NULL");
+    int64_t z_lo, nzr;
+    rank_planes(c, &z_lo, &nzr);
+    const int64_t per_field = nzr * c->plane;
+    if (count != c->F * per_field)
+        return fail(c, GBS_E_INVAL, "count=%lld, expected F*slab points=%lld", (long long)count,
+                    (long long)(c->F * per_field));
+    CU(c, cudaSetDevice(c->device));
+    int rc;
+    if ((rc = async_setup(c))) return rc;
+    if ((rc = consume_in(c))) return rc;            // an earlier staged state lands first
+    CU(c, cudaStreamWaitEvent(c->h2d, c->ev_in_free, 0));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (size_t v = 0; v < c->slab.size(); ++v) {
+        Slab& s = c->slab[v];
+        const int64_t n = s.nz * c->plane;
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(c->in_buf[v] + (int64_t)f * n, src + (int64_t)f * per_field + (s.z0 - z_lo) * c->plane,
+                                  sizeof(double) * (size_t)n, kind, c->h2d));
+    }
+    CU(c, cudaEventRecord(c->ev_in_ready, c->h2d));
+    c->pending_in = true;
+    c->have_state = true;
+    return GBS_OK;
+}
+
+int gbs_read_slab_async(gbs_ctx* c, double* dst, int64_t count, int on_device) {
+    if (!c || !dst) return fail(c, GBS_E_INVAL, "ctx or dst is NULL");
+    if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_read_slab_async before a state was written");
+    int64_t z_lo, nzr;
+    rank_planes(c, &z_lo, &nzr);
+    const int64_t per_field = nzr * c->plane;
+    if (count != c->F * per_field)
+        return fail(c, GBS_E_INVAL, "count=%lld, expected F*slab points=%lld", (long long)count,
+                    (long long)(c->F * per_field));
+    CU(c, cudaSetDevice(c->device));
+    int rc;
+    if ((rc = async_setup(c))) return rc;
+    if ((rc = consume_in(c))) return rc;
+    // snapshot Y into the outgoing staging buffer (context stream), then copy it out (d2h)
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_out_free, 0));
+    for (size_t v = 0; v < c->slab.size(); ++v) {
+        Slab& s = c->slab[v];
+        const int64_t n = s.nz * c->plane;
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(c->out_buf[v] + (int64_t)f * n, field_ptr(c, s, c->yb, f),
+                                  sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CU(c, cudaEventRecord(c->ev_out_ready, c->stream));
+    CU(c, cudaStreamWaitEvent(c->d2h, c->ev_out_ready, 0));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    for (size_t v = 0; v < c->slab.size(); ++v) {
+        Slab& s = c->slab[v];
+        const int64_t n = s.nz * c->plane;
+        for (int f = 0; f < c->F; ++f)
+            CU(c, cudaMemcpyAsync(dst + (int64_t)f * per_field + (s.z0 - z_lo) * c->plane, c->out_buf[v] + (int64_t)f * n,
+                                  sizeof(double) * (size_t)n, kind, c->d2h));
+    }
+    CU(c, cudaEventRecord(c->ev_out_free, c->d2h));
+    return GBS_OK;
 }
 
 int gbs_query(const gbs_ctx* c, gbs_info* info) {

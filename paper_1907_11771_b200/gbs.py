@@ -26,7 +26,7 @@ FIELDS = {"adv1d": 1, "acoustic2d": 3, "wave3d": 2}
 NDIM = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
 
 EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_write_slab",
-           "gbs_read_slab", "gbs_sync",
+           "gbs_read_slab", "gbs_write_slab_async", "gbs_read_slab_async", "gbs_sync",
            "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
            "gbs_set_option",
            "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
@@ -109,6 +109,8 @@ def load(build_if_missing: bool = False):
     L.gbs_read_state.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_write_slab.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_read_slab.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_write_slab_async.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_read_slab_async.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_sync.argtypes = [vp]
     L.gbs_destroy.argtypes = [vp]
     L.gbs_destroy.restype = None
@@ -238,6 +240,18 @@ def gbs_read_slab(ctx, dst) -> None:
     _check(load().gbs_read_slab(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
 
 
+def gbs_write_slab_async(ctx, src) -> None:
+    """Stage src (keep it alive and unmodified until gbs_sync) as the next state."""
+    p, dev, cnt = _ptr_and_device(src)
+    _check(load().gbs_write_slab_async(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
+
+
+def gbs_read_slab_async(ctx, dst) -> None:
+    """Queue a copy of the current state into dst (complete after gbs_sync)."""
+    p, dev, cnt = _ptr_and_device(dst)
+    _check(load().gbs_read_slab_async(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
+
+
 def gbs_sync(ctx) -> None:
     _check(load().gbs_sync(ctx), ctx)
 
@@ -297,6 +311,16 @@ class Stepper:
     def read_slab(self, out):
         gbs_read_slab(self.ctx, out)
         return out
+
+    def write_async(self, y):
+        gbs_write_slab_async(self.ctx, y)
+
+    def read_async(self, out):
+        gbs_read_slab_async(self.ctx, out)
+        return out
+
+    def sync(self):
+        gbs_sync(self.ctx)
 
     def info(self):
         return gbs_query(self.ctx)
