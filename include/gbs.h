@@ -227,7 +227,10 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *   "fuse"         1/0   two substeps per HBM pass on TMA grids (default 1)
  *   "persistent"   1/0   1-D grids up to 7000 points with m <= 16: every macro step of
  *                        a gbs_advance in one thread-block-cluster launch (default 1)
- *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)  */
+ *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)
+ *   "overlap"      1/0   slabbed layouts: exchange the ghost planes on a comm stream
+ *                        while the interior planes are computed, then the face bands
+ *                        (default 1)  */
 GBS_API int gbs_set_option(gbs_ctx* ctx, const char* key, int64_t value);
 
 /* Accumulated device time (ms) and launch count of the timed kernels of a class

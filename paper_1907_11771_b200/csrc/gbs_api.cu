@@ -166,6 +166,10 @@ struct gbs_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr, ev_out_ready = nullptr, ev_out_free = nullptr;
     bool pending_in = false;
+    // halo exchange overlapped with the interior planes (slabbed layouts)
+    bool use_overlap = true;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
     double* d_wh = nullptr;
     bool use_fuse = true;             // two-substep (temporally blocked) kernels where eligible
@@ -286,6 +290,10 @@ static void plan(gbs_ctx* c, int want_groups) {
         double t_comp = crit * pts * 24.0 * c->F / 6.5e12;
         double halo_fields = c->pde == GBS_WAVE3D ? 1.0 : 2.0;
         double t_halo = s > 1 ? crit * (2.0 * c->R * c->plane * 8.0 * halo_fields / 7.7e11 + 2e-5) : 0.0;
+        // the exchange overlaps the interior planes; only what exceeds them is exposed
+        const double nzs = (double)c->nslow / s;
+        if (s > 1 && c->use_overlap && nzs >= 3.0 * 16.0)
+            t_halo = std::max(0.0, t_halo - t_comp * (nzs - 2.0 * 16.0) / nzs);
         double state = pts * c->F * 8.0;
         double t_ar = g > 1 ? 2.0 * (g - 1) / g * state / 7.0e11 + 5e-5 : 0.0;
         double tot = t_comp + t_halo + t_ar;
@@ -444,7 +452,8 @@ static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
     return (int)((extent + chunks - 1) / chunks);
 }
 
-static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
+// one substep over the planes [lo, hi) of slab s (lo = 0, hi = s.nz: the whole slab)
+static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi) {
     const bool slab = c->ghost > 0;
     int* flag = op.flag ? c->d_flag : nullptr;
     if (c->pde == GBS_WAVE3D) {
@@ -462,9 +471,10 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         const bool vx2 = (c->n[0] % 2) == 0;
         if (c->use_bulk && s.tma_ok) {
             int64_t tx = c->n[0] / gbs::tma::TX, ty = c->n[1] / gbs::tma::TY;
-            a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, s.nz)
-                                         : (int)std::min<int64_t>(128, s.nz);
-            dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
+            a.zlo = (int)lo; a.zhi = (int)hi;
+            a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo)
+                                         : (int)std::min<int64_t>(128, hi - lo);
+            dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
             gbs::tma::Maps m;
             m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
             m.sv = s.tm[op.S][1][0];
@@ -490,8 +500,9 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         }
         const int TX = vx2 ? 64 : 32, TY = 16;
         int64_t tx = (c->n[0] + TX - 1) / TX, ty = (c->n[1] + TY - 1) / TY;
-        a.zchunk = chunk_for(tx * ty, s.nz, c->zchunk_opt);
-        dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
+        a.zlo = (int)lo; a.zhi = (int)hi;
+        a.zchunk = chunk_for(tx * ty, hi - lo, c->zchunk_opt);
+        dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
 #define W3(RR, SL)                                                                   \
         switch (op.mode) {                                                           \
             case gbs::MODE_FE: launch_wave3d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
@@ -514,8 +525,9 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
         if (c->use_bulk && s.tma_ok) {
             const int64_t xt = c->n[0] / gbs::tma::TX;
-            a.ychunk = ac2d_ychunk(xt, s.nz, c->zchunk_opt, c->sms);
-            dim3 grid((unsigned)xt, (unsigned)((s.nz + a.ychunk - 1) / a.ychunk));
+            a.ylo = (int)lo; a.yhi = (int)hi;
+            a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms);
+            dim3 grid((unsigned)xt, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
             gbs::tma::AcMaps m;
             for (int f = 0; f < 3; ++f) {
                 m.s_a[f] = s.tm[op.S][f][0]; m.s_b[f] = s.tm[op.S][f][1]; m.s_c[f] = s.tm[op.S][f][2];
@@ -543,8 +555,9 @@ static int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op) {
         const bool vx2 = (c->n[0] % 2) == 0;
         const int TX = vx2 ? 256 : 128;
         int64_t tx = (c->n[0] + TX - 1) / TX;
-        a.ychunk = chunk_for(tx, s.nz, c->zchunk_opt);
-        dim3 grid((unsigned)tx, (unsigned)((s.nz + a.ychunk - 1) / a.ychunk));
+        a.ylo = (int)lo; a.yhi = (int)hi;
+        a.ychunk = chunk_for(tx, hi - lo, c->zchunk_opt);
+        dim3 grid((unsigned)tx, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
 #define A2(RR, SL)                                                                   \
         switch (op.mode) {                                                           \
             case gbs::MODE_FE: launch_ac2d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
@@ -591,7 +604,7 @@ struct PairOperands {
     bool flag;
 };
 
-static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
+static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi) {
     const bool slab = c->ghost > 0;
     const bool lf = op.modeB == gbs::MODE_LF;
     gbs::tma::PairArgs a;
@@ -611,9 +624,10 @@ static int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op) {
     a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
     a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
     a.nonfinite = op.flag ? c->d_flag : nullptr;
-    a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, s.nz) : (int)std::min<int64_t>(128, s.nz);
+    a.zlo = (int)lo; a.zhi = (int)hi;
+    a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo) : (int)std::min<int64_t>(128, hi - lo);
     dim3 grid((unsigned)(c->n[0] / gbs::tma::TX), (unsigned)(c->n[1] / gbs::tma::TY),
-              (unsigned)((s.nz + a.zchunk - 1) / a.zchunk));
+              (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
     gbs::tma::PairMaps m;
     m.su_a = s.tm[op.Su.b][op.Su.f][0]; m.su_b = s.tm[op.Su.b][op.Su.f][1]; m.su_c = s.tm[op.Su.b][op.Su.f][2];
     m.u_a = s.tm[op.U.b][op.U.f][0]; m.u_b = s.tm[op.U.b][op.U.f][1]; m.u_c = s.tm[op.U.b][op.U.f][2];
@@ -666,7 +680,8 @@ static std::vector<gbs_halo_op> halo_schedule(int slabs, int my_slab, int64_t nz
 // halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
 // whose stencil crosses the slab axis) -- ghost planes along the slowest axis
 // ---------------------------------------------------------------------------
-static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0) {
+static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
     if (c->ghost == 0) return GBS_OK;
     const int64_t G = c->ghost, P = c->plane;
     const size_t cnt = (size_t)(G * P);
@@ -691,10 +706,10 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0) {
                 double* mine = field_ptr(c, me, b, f);
                 // bottom ghosts <- lower neighbour's top interior planes
                 CU(c, cudaMemcpyAsync(mine - G * P, field_ptr(c, lo, b, f) + (lo.nz - G) * P,
-                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
                 // top ghosts <- upper neighbour's bottom interior planes
                 CU(c, cudaMemcpyAsync(mine + me.nz * P, field_ptr(c, hi, b, f),
-                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
             }
         }
         return GBS_OK;
@@ -711,8 +726,8 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0) {
     for (const auto& op : ops) {
         double* p = field_ptr(c, me, b, op.field) + op.plane0 * P;
         const size_t n = (size_t)(op.planes * P);
-        if (op.kind == 0) NC(c, A.Send(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, c->stream));
-        else NC(c, A.Recv(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, c->stream));
+        if (op.kind == 0) NC(c, A.Send(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, st));
+        else NC(c, A.Recv(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, st));
     }
     NC(c, A.GroupEnd());
     return GBS_OK;
@@ -738,26 +753,84 @@ static int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev) {
     return GBS_OK;
 }
 
+// Planes next to a slab face need the ghost planes; the rest do not.  With slabs the
+// halo exchange runs on the context's comm stream while the interior planes are computed
+// on the context stream, and the two face bands follow once the exchange is in (event
+// fork / join, also inside the captured graph).  B = the face band thickness.
+static int64_t face_band(const gbs_ctx* c, const Slab& s) {
+    if (c->pde == GBS_ACOUSTIC2D && c->use_bulk && s.tma_ok) return gbs::tma::TY;   // whole 16-row bands
+    return c->R;
+}
+
+static bool overlap_halo(gbs_ctx* c) {
+    if (c->ghost == 0 || !c->use_overlap) return false;
+    for (const auto& s : c->slab)
+        if (s.nz < 3 * face_band(c, s)) return false;
+    return true;
+}
+
+static int comm_fork(gbs_ctx* c) {
+    if (!c->cstream) {
+        CU(c, cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        CU(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CU(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    CU(c, cudaEventRecord(c->ev_fork, c->stream));
+    CU(c, cudaStreamWaitEvent(c->cstream, c->ev_fork, 0));
+    return GBS_OK;
+}
+
+static int comm_join(gbs_ctx* c) {
+    CU(c, cudaEventRecord(c->ev_join, c->cstream));
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    return GBS_OK;
+}
+
+template <typename Launch>
+static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pair<int, unsigned>>& halos) {
+    int rc;
+    if (!overlap_halo(c)) {
+        for (auto& h : halos)
+            if ((rc = exchange_halo(c, h.first, h.second))) return rc;
+        for (auto& s : c->slab)
+            if ((rc = launch(s, (int64_t)0, s.nz))) return rc;
+        return GBS_OK;
+    }
+    if ((rc = comm_fork(c))) return rc;
+    for (auto& h : halos)
+        if ((rc = exchange_halo(c, h.first, h.second, c->cstream))) return rc;
+    for (auto& s : c->slab) {
+        const int64_t B = face_band(c, s);
+        if ((rc = launch(s, B, s.nz - B))) return rc;                  // interior: no ghosts read
+    }
+    if ((rc = comm_join(c))) return rc;
+    for (auto& s : c->slab) {
+        const int64_t B = face_band(c, s);
+        if ((rc = launch(s, (int64_t)0, B))) return rc;
+        if ((rc = launch(s, s.nz - B, s.nz))) return rc;
+    }
+    return GBS_OK;
+}
+
 static int step(gbs_ctx* c, int cls, const StepOperands& op) {
     int rc;
-    if ((rc = exchange_halo(c, op.S))) return rc;
     cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
-    for (auto& s : c->slab)
-        if ((rc = launch_step(c, s, op))) return rc;
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_step(c, s, op, lo, hi); },
+                        {{op.S, 0u}});
+    if (rc) return rc;
     if (end) CU(c, cudaEventRecord(end, c->stream));
     return GBS_OK;
 }
 
 static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
     int rc;
-    // the pair kernel reads S_u and U with stencils
-    if ((rc = exchange_halo(c, op.Su.b, 1u << op.Su.f))) return rc;
-    if ((rc = exchange_halo(c, op.U.b, 1u << op.U.f))) return rc;
     cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
-    for (auto& s : c->slab)
-        if ((rc = launch_pair(c, s, op))) return rc;
+    // the pair kernel reads S_u and U with stencils
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_pair(c, s, op, lo, hi); },
+                        {{op.Su.b, 1u << op.Su.f}, {op.U.b, 1u << op.U.f}});
+    if (rc) return rc;
     if (end) CU(c, cudaEventRecord(end, c->stream));
     return GBS_OK;
 }
@@ -1049,6 +1122,9 @@ void gbs_destroy(gbs_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->h2d) { cudaStreamSynchronize(c->h2d); cudaStreamDestroy(c->h2d); }
+    if (c->cstream) { cudaStreamSynchronize(c->cstream); cudaStreamDestroy(c->cstream); }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->d2h) { cudaStreamSynchronize(c->d2h); cudaStreamDestroy(c->d2h); }
     for (cudaEvent_t e : {c->ev_in_ready, c->ev_in_free, c->ev_out_ready, c->ev_out_free})
         if (e) cudaEventDestroy(e);
@@ -1257,6 +1333,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     };
     if (k == "graph") { c->use_graph = value != 0 && c->world == 1; drop_graphs(); return GBS_OK; }
     if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "overlap") { c->use_overlap = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }

@@ -105,6 +105,7 @@ struct Wave3DArgs {
     double* Ou; double* Ov;
     int nx, ny, nz;          // local extents (nz = local slab thickness)
     int zchunk;
+    int zlo, zhi;            // planes [zlo, zhi) of the slab this launch computes
     int64_t plane;           // nx * ny
     double sx2, sy2, sz2;    // squared inverse spacings
     double cf, wh;
@@ -129,8 +130,8 @@ wave3d_step(const Wave3DArgs A) {
     const int tx = threadIdx.x, ty = threadIdx.y, t = ty * 32 + tx;
     const int nx = A.nx, ny = A.ny, nz = A.nz;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = blockIdx.z * A.zchunk;
-    const int z1 = min(z0 + A.zchunk, nz);
+    const int z0 = A.zlo + blockIdx.z * A.zchunk;
+    const int z1 = min(z0 + A.zchunk, A.zhi);
     const int64_t plane = A.plane;
 
     const int gx = wrap_any(x0 + tx * VX, nx);
@@ -252,6 +253,7 @@ struct Acoustic2DArgs {
     double* O[3];
     int nx, ny;              // local extents (ny = local slab thickness)
     int ychunk;
+    int ylo, yhi;            // rows [ylo, yhi) of the slab this launch computes
     double sx, sy;           // inverse spacings
     double cf, wh;
     int* nonfinite;
@@ -270,8 +272,8 @@ acoustic2d_step(const Acoustic2DArgs A) {
     const int tx = threadIdx.x;
     const int nx = A.nx, ny = A.ny;
     const int x0 = blockIdx.x * TX;
-    const int ys = blockIdx.y * A.ychunk;
-    const int ye = min(ys + A.ychunk, ny);
+    const int ys = A.ylo + blockIdx.y * A.ychunk;
+    const int ye = min(ys + A.ychunk, A.yhi);
     const int gx = wrap_any(x0 + tx * VX, nx);
     const bool valid = x0 + tx * VX < nx;
     // x-halo: threads 0..4R-1 load p (0..2R-1) and u (2R..4R-1) halo columns

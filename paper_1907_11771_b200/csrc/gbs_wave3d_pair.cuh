@@ -73,6 +73,7 @@ struct PairArgs {
     double* Cu;                       // u_{n+3} (LF)
     const double* Su; const double* U;
     int nx, ny, nz, zchunk;
+    int zlo, zhi;                     // planes [zlo, zhi) of the slab this launch computes
     int64_t plane;
     double sx2, sy2, sz2;
     double cfA, cfB, wh;
@@ -94,8 +95,8 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
     const int nx = A.nx, ny = A.ny, nz = A.nz;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = blockIdx.z * A.zchunk;
-    const int niter = min(A.zchunk, nz - z0);
+    const int z0 = A.zlo + blockIdx.z * A.zchunk;
+    const int niter = min(A.zchunk, A.zhi - z0);
     auto zc = [&](int z) -> int {
         if constexpr (SLAB) return z + zbase;
         else return wrap_once(z, nz);

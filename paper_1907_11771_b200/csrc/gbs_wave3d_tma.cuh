@@ -113,8 +113,8 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
     // x-tiles vary fastest in the launch order: resident CTAs stream whole rows
     // (DRAM page locality; y-fastest order measured 10% slower on 1024^3)
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = blockIdx.z * A.zchunk;
-    const int niter = min(A.zchunk, nz - z0);
+    const int z0 = A.zlo + blockIdx.z * A.zchunk;
+    const int niter = min(A.zchunk, A.zhi - z0);
 
     auto zc = [&](int z) -> int {              // tensor z coordinate of logical plane z
         if constexpr (SLAB) return z + zbase;

@@ -361,6 +361,23 @@ def test_loopback_slabs(torch_cuda, cfg, n, slabs):
     assert_parity(g[0], o[0], what=f"loopback {slabs}")
 
 
+@pytest.mark.parametrize("cfg,n,slabs", [("c4", (64, 32, 48), 2), ("c5", (64, 48, 60), 3),
+                                         ("c4", (40, 36, 36), 3), ("c2", (128, 96, 1), 2),
+                                         ("c3", (200, 72, 1), 3)])
+def test_halo_overlap_is_bitwise_identical(torch_cuda, cfg, n, slabs):
+    """Slabbed layouts exchange the halo on a comm stream while the interior planes are
+    computed, then compute the face bands (option overlap, default on): the same bytes as
+    exchanging first, with and without graph capture, and the oracle's result."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": 1})
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": 0})
+    _, c, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": 1, "graph": 0})
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[0], c[0])
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(a[0], o[0], what=f"overlap {cfg} {slabs} slabs")
+
+
 # ----------------------------------------------------------------------------- errors
 def test_error_paths(torch_cuda):
     gbs = gbs_mod()
