@@ -88,6 +88,22 @@ def test_plan_balances_like_the_paper():
     assert plans[0]["critical_substeps"] == 12
 
 
+@pytest.mark.parametrize("cores,nmax", [(6, 22), (8, 30)])
+def test_plan_folds_the_papers_multicore_schemes(cores, nmax):
+    """§3.6: with N_max = 4 n_cores - 2, the counts {2..N_max} fold onto
+    n_cores cores as {N_max} and pairs summing to N_max -- GBS_8,6 on 6 GPUs, GBS_8,8 on 8
+    (SURVEY.md §8(f) NEXT-1).  Without the shared first evaluation a pair costs N_max + 2."""
+    assert nmax == 4 * cores - 2
+    counts = list(range(2, nmax + 1, 2))
+    plans = [gbs.gbs_plan("wave3d", (64, 64, 64), 8, counts, cores, r, cores) for r in range(cores)]
+    groups = sorted(sorted(p["my_n_k"]) for p in plans)
+    assert [nmax] in groups
+    pairs = [g for g in groups if g != [nmax]]
+    assert len(pairs) == cores - 1 and all(len(g) == 2 and sum(g) == nmax for g in pairs)
+    assert sorted(n for g in groups for n in g) == counts
+    assert plans[0]["critical_substeps"] == nmax + 2
+
+
 # --------------------------------------------------------------------------- gloo, multi-process
 def _halo_worker(rank, world, nz_local, ghost, nfields):
     """Each rank = one slab of a periodic z axis; global plane index in every value."""
