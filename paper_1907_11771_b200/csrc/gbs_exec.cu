@@ -1,0 +1,318 @@
+// gbs_exec.cu -- the schedule of one macro step (Eq. (1), lines 85-98,
+// and the combination at lines 109-115, 221-225), per local slab:
+//   for each sequence k of this rank's group, ascending n_k, h = H / n_k:
+//     FE, n_k leap-frog steps, the final step fused with the averaging and the
+//     weighted accumulate -- single-substep launches, or (3-D TMA grids) FE and
+//     n_k/2 two-substep launches
+//   [multi-GPU] ACC <- sum over sequence groups        (ncclAllReduce, fp64 sum)
+//   swap(Y, ACC)
+// On slabbed layouts the ghost planes of every stencil operand are refreshed
+// before each launch (device copies between local slabs in loopback mode,
+// ncclSend/ncclRecv between ranks), overlapped with the interior planes.
+// gbs_advance replays the macro step as a CUDA graph.
+#include "gbs_internal.h"
+#include "gbs_wave3d_tma.cuh"     // substep modes and the TMA tile (no launches here)
+
+// ---------------------------------------------------------------------------
+// halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
+// whose stencil crosses the slab axis) -- ghost planes along the slowest axis
+// ---------------------------------------------------------------------------
+static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
+    if (c->ghost == 0) return GBS_OK;
+    const int64_t G = c->ghost, P = c->plane;
+    const size_t cnt = (size_t)(G * P);
+    std::vector<int> fields;
+    if (mask) {
+        for (int f = 0; f < c->F; ++f)
+            if (mask & (1u << f)) fields.push_back(f);
+    } else if (c->pde == GBS_WAVE3D) {
+        fields = {0};
+    } else {
+        fields = {0, 2};                        // acoustics: p and v cross the y slabs
+    }
+    const int nloc = c->loopback;
+    const int S = c->slabs * nloc;              // global slab count
+    if (c->slabs == 1) {
+        // all slabs local: device-to-device copies
+        for (int v = 0; v < nloc; ++v) {
+            Slab& me = c->slab[v];
+            Slab& lo = c->slab[(v - 1 + nloc) % nloc];
+            Slab& hi = c->slab[(v + 1) % nloc];
+            for (int f : fields) {
+                double* mine = field_ptr(c, me, b, f);
+                // bottom ghosts <- lower neighbour's top interior planes
+                CU(c, cudaMemcpyAsync(mine - G * P, field_ptr(c, lo, b, f) + (lo.nz - G) * P,
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                // top ghosts <- upper neighbour's bottom interior planes
+                CU(c, cudaMemcpyAsync(mine + me.nz * P, field_ptr(c, hi, b, f),
+                                      cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        return GBS_OK;
+    }
+    if (nloc != 1) return fail(c, GBS_E_UNSUPPORTED, "loopback slabs with multi-GPU slabs");
+    (void)S;
+    (void)cnt;
+    auto& A = nccl::api();
+    Slab& me = c->slab[0];
+    unsigned fm = 0;
+    for (int f : fields) fm |= 1u << f;
+    const std::vector<gbs_halo_op> ops = halo_schedule(c->slabs, c->my_slab, me.nz, (int)G, fm);
+    NC(c, A.GroupStart());
+    for (const auto& op : ops) {
+        double* p = field_ptr(c, me, b, op.field) + op.plane0 * P;
+        const size_t n = (size_t)(op.planes * P);
+        if (op.kind == 0) NC(c, A.Send(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, st));
+        else NC(c, A.Recv(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, st));
+    }
+    NC(c, A.GroupEnd());
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// timing instrumentation (event pairs on the context stream)
+// ---------------------------------------------------------------------------
+int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev) {
+    KernelTimer& T = c->timer;
+    if (T.used + 2 > T.ev.size()) {
+        for (int i = 0; i < 256; ++i) {
+            cudaEvent_t e;
+            CU(c, cudaEventCreate(&e));
+            T.ev.push_back(e);
+        }
+        T.cls.resize(T.ev.size() / 2);
+    }
+    CU(c, cudaEventRecord(T.ev[T.used], c->stream));
+    T.cls[T.used / 2] = cls;
+    *end_ev = T.ev[T.used + 1];
+    T.used += 2;
+    return GBS_OK;
+}
+
+// Planes next to a slab face need the ghost planes; the rest do not.  With slabs the
+// halo exchange runs on the context's comm stream while the interior planes are computed
+// on the context stream, and the two face bands follow once the exchange is in (event
+// fork / join, also inside the captured graph).  B = the face band thickness.
+static int64_t face_band(const gbs_ctx* c, const Slab& s) {
+    if (c->pde == GBS_ACOUSTIC2D && c->use_bulk && s.tma_ok) return gbs::tma::TY;   // whole 16-row bands
+    return c->R;
+}
+
+static bool overlap_halo(gbs_ctx* c) {
+    if (c->ghost == 0 || !c->use_overlap) return false;
+    for (const auto& s : c->slab)
+        if (s.nz < 3 * face_band(c, s)) return false;
+    return true;
+}
+
+static int comm_fork(gbs_ctx* c) {
+    if (!c->cstream) {
+        CU(c, cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        CU(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CU(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    CU(c, cudaEventRecord(c->ev_fork, c->stream));
+    CU(c, cudaStreamWaitEvent(c->cstream, c->ev_fork, 0));
+    return GBS_OK;
+}
+
+static int comm_join(gbs_ctx* c) {
+    CU(c, cudaEventRecord(c->ev_join, c->cstream));
+    CU(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    return GBS_OK;
+}
+
+template <typename Launch>
+static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pair<int, unsigned>>& halos) {
+    int rc;
+    if (!overlap_halo(c)) {
+        for (auto& h : halos)
+            if ((rc = exchange_halo(c, h.first, h.second))) return rc;
+        for (auto& s : c->slab)
+            if ((rc = launch(s, (int64_t)0, s.nz))) return rc;
+        return GBS_OK;
+    }
+    if ((rc = comm_fork(c))) return rc;
+    for (auto& h : halos)
+        if ((rc = exchange_halo(c, h.first, h.second, c->cstream))) return rc;
+    for (auto& s : c->slab) {
+        const int64_t B = face_band(c, s);
+        if ((rc = launch(s, B, s.nz - B))) return rc;                  // interior: no ghosts read
+    }
+    if ((rc = comm_join(c))) return rc;
+    for (auto& s : c->slab) {
+        const int64_t B = face_band(c, s);
+        if ((rc = launch(s, (int64_t)0, B))) return rc;
+        if ((rc = launch(s, s.nz - B, s.nz))) return rc;
+    }
+    return GBS_OK;
+}
+
+static int step(gbs_ctx* c, int cls, const StepOperands& op) {
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_step(c, s, op, lo, hi); },
+                        {{op.S, 0u}});
+    if (rc) return rc;
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    return GBS_OK;
+}
+
+static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
+    // the pair kernel reads S_u and U with stencils
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_pair(c, s, op, lo, hi); },
+                        {{op.Su.b, 1u << op.Su.f}, {op.U.b, 1u << op.U.f}});
+    if (rc) return rc;
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    return GBS_OK;
+}
+
+static bool fused_path(const gbs_ctx* c) {
+    if (!(c->use_fuse && c->use_bulk && c->nbuf == 6)) return false;
+    for (const auto& s : c->slab)
+        if (!s.tma_ok) return false;
+    return true;
+}
+
+int harvest_timer(gbs_ctx* c) {
+    KernelTimer& T = c->timer;
+    if (!T.used) return GBS_OK;
+    CU(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < T.used; i += 2) {
+        float ms = 0.f;
+        CU(c, cudaEventElapsedTime(&ms, T.ev[i], T.ev[i + 1]));
+        int k = T.cls[i / 2];
+        T.total_ms[k] += ms;
+        T.launches[k] += 1;
+    }
+    T.used = 0;
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one macro step (enqueue only)
+// ---------------------------------------------------------------------------
+static int enqueue_macro(gbs_ctx* c, double H) {
+    const int Y = c->yb, ACC = 1 - c->yb, B = 2, C = 3;
+    const int64_t l0 = c->launches;
+    int rc;
+    bool first = true;
+    const bool fused = fused_path(c);
+    for (size_t q = 0; q < c->my_seq.size(); ++q) {
+        const int k = c->my_seq[q];
+        const int n = c->nk_all[k];
+        const double h = H / (double)n;
+        const bool last = (q + 1 == c->my_seq.size());
+        if (fused) {
+            // FE (which also forms u_2), then n/2 launches of two substeps:
+            // (LF1, LF2), ..., (LF_{n-1}, final).  Field slots: y1 -> buffer 2; the
+            // u-levels rotate through (2,0)/(3,0) and (4,0)/(5,0); v_{odd} stays in
+            // (2,1) and v_{even} in (3,1), both updated in place (pointwise reads).
+            StepOperands fe{Y, Y, 2, gbs::MODE_FE, h, 0.0, false};
+            fe.xu = Slot{3, 0};
+            fe.cf2 = 2.0 * h;
+            if ((rc = step(c, 1, fe))) return rc;                                            // y1, u2
+            Slot Pv{Y, 1}, Su{2, 0}, Sv{2, 1}, U{3, 0};
+            for (int p = 0; p < n / 2; ++p) {
+                if (p + 1 < n / 2) {
+                    const int nb = Su.b == 2 ? 4 : 2;
+                    PairOperands op{Pv, Su, Sv, U, Slot{3, 1}, Slot{nb, 0}, Sv, Slot{nb + 1, 0},
+                                    gbs::MODE_LF, 2.0 * h, 2.0 * h, 0.0, false};
+                    if ((rc = pair_step(c, 3, op))) return rc;
+                    Pv = Slot{3, 1}; Su = Slot{nb, 0}; U = Slot{nb + 1, 0};
+                } else {
+                    PairOperands fin{Pv, Su, Sv, U, Slot{ACC, 0}, Slot{ACC, 0}, Slot{ACC, 1}, Slot{ACC, 0},
+                                     first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, 2.0 * h, h,
+                                     0.5 * c->wk_all[k], last};
+                    if ((rc = pair_step(c, 4, fin))) return rc;
+                }
+            }
+            first = false;
+            continue;
+        }
+        if ((rc = step(c, 1, {Y, Y, B, gbs::MODE_FE, h, 0.0, false}))) return rc;            // y1
+        if ((rc = step(c, 0, {B, Y, C, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;      // y2
+        int prev = B, cur = C;
+        for (int i = 2; i <= n - 1; ++i) {                                                    // y3..yN
+            if ((rc = step(c, 0, {cur, prev, prev, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;
+            std::swap(prev, cur);
+        }
+        StepOperands fin{cur, prev, ACC, first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, h,
+                         0.5 * c->wk_all[k], last};
+        if ((rc = step(c, 2, fin))) return rc;
+        first = false;
+    }
+    if (c->groups > 1) {
+        auto& A = nccl::api();
+        Slab& s = c->slab[0];
+        NC(c, A.GroupStart());
+        for (int f = 0; f < c->F; ++f) {
+            double* p = field_ptr(c, s, ACC, f);
+            NC(c, A.AllReduce(p, p, (size_t)(s.nz * c->plane), nccl::ncclFloat64, nccl::ncclSum,
+                              c->comm_group, c->stream));
+        }
+        NC(c, A.GroupEnd());
+    }
+    c->yb = ACC;
+    c->launches_per_macro = c->launches - l0;
+    return GBS_OK;
+}
+
+extern "C" {
+
+int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
+    if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_advance before gbs_write_state");
+    if (macro_steps < 0) return fail(c, GBS_E_INVAL, "macro_steps=%lld < 0", (long long)macro_steps);
+    if (!(H > 0.0) || !std::isfinite(H)) return fail(c, GBS_E_INVAL, "H=%g must be positive and finite", H);
+    CU(c, cudaSetDevice(c->device));
+    int rc;
+    if ((rc = consume_in(c))) return rc;
+    if (macro_steps > 0 && persistent_path(c)) {
+        if ((rc = launch_cluster_run(c, macro_steps, H))) return rc;
+        c->macro_done += macro_steps;
+        c->t += H * (double)macro_steps;
+        return GBS_OK;
+    }
+    if (c->order == 0)
+        return fail(c, GBS_E_UNSUPPORTED, "the spectral derivative runs only in the cluster kernel "
+                                          "(one GPU, no loopback, option persistent=1)");
+    const bool graph = c->use_graph && !c->time_kernels && macro_steps > 0;
+    if (graph && c->graph_H != H) {
+        for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+        c->graph_H = H;
+    }
+    for (int64_t i = 0; i < macro_steps; ++i) {
+        if (graph) {
+            const int par = c->yb;
+            if (!c->gexec[par]) {
+                cudaGraph_t gr;
+                CU(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+                rc = enqueue_macro(c, H);
+                cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+                if (rc) { if (e == cudaSuccess) cudaGraphDestroy(gr); return rc; }
+                if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+                e = cudaGraphInstantiate(&c->gexec[par], gr, 0);
+                cudaGraphDestroy(gr);
+                if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+                c->yb = par;          // capture does not execute: rewind the parity
+                c->launches -= c->launches_per_macro;
+            }
+            CU(c, cudaGraphLaunch(c->gexec[par], c->stream));
+            c->launches += c->launches_per_macro;
+            c->yb = 1 - par;
+        } else {
+            if ((rc = enqueue_macro(c, H))) return rc;
+        }
+        c->macro_done++;
+        c->t += H;
+    }
+    return GBS_OK;
+}
+
+}  // extern "C"

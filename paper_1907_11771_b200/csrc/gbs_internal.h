@@ -1,0 +1,204 @@
+// gbs_internal.h -- state and helpers shared by the translation units of
+// libgbs_b200.so (not part of the C ABI; every symbol here has hidden
+// visibility).  gbs_api.cu: context lifetime, options, queries; gbs_plan.cu:
+// validation, the sequence-group x slab planner, the halo schedule;
+// gbs_launch.cu: device memory, tensor maps and every kernel launch;
+// gbs_exec.cu: the macro-step schedule (halo exchange, comm/compute overlap,
+// CUDA graphs); gbs_io.cu: synchronous and asynchronous state IO.
+#pragma once
+
+#include "gbs.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time from the process (torch's libnccl.so.2) so the
+// library loads on machines without NCCL and never links a second copy.
+// ---------------------------------------------------------------------------
+namespace nccl {
+typedef struct ncclComm* comm_t;
+typedef struct { char internal[128]; } uid_t;
+enum { ncclSuccess = 0 };
+enum { ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+typedef int (*GetUniqueId_t)(uid_t*);
+typedef int (*CommInitRank_t)(comm_t*, int, uid_t, int);
+typedef int (*CommSplit_t)(comm_t, int, int, comm_t*, void*);
+typedef int (*CommDestroy_t)(comm_t);
+typedef int (*AllReduce_t)(const void*, void*, size_t, int, int, comm_t, cudaStream_t);
+typedef int (*AllGather_t)(const void*, void*, size_t, int, comm_t, cudaStream_t);
+typedef int (*Send_t)(const void*, size_t, int, int, comm_t, cudaStream_t);
+typedef int (*Recv_t)(void*, size_t, int, int, comm_t, cudaStream_t);
+typedef int (*Group_t)(void);
+typedef const char* (*GetErrorString_t)(int);
+struct Api {
+    bool ok = false;
+    GetUniqueId_t GetUniqueId; CommInitRank_t CommInitRank; CommSplit_t CommSplit;
+    CommDestroy_t CommDestroy; AllReduce_t AllReduce; AllGather_t AllGather;
+    Send_t Send; Recv_t Recv; Group_t GroupStart, GroupEnd; GetErrorString_t GetErrorString;
+};
+Api& api();                        // gbs_api.cu
+}  // namespace nccl
+
+// ---------------------------------------------------------------------------
+struct Slab {
+    int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
+    double* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // Y, ACC, L0..L3 (+ ghosts)
+    bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
+    CUtensorMap tm[6][3][3];          // [buffer][field][box shape A/B/C] (TMA kernels)
+};
+
+constexpr int kClusterMaxN = 7000;     // 4 nx doubles of shared memory per CTA
+constexpr int kSpectralMaxN = 6400;    // 4.5 nx doubles (state, levels, weights)
+
+struct KernelTimer {
+    std::vector<cudaEvent_t> ev;      // pairs
+    std::vector<int> cls;
+    size_t used = 0;
+    double total_ms[6] = {0, 0, 0, 0, 0, 0};
+    int64_t launches[6] = {0, 0, 0, 0, 0, 0};
+};
+
+struct gbs_ctx {
+    // problem
+    int pde = 0, ndim = 0, F = 0, order = 0, R = 0;
+    int64_t n[3] = {1, 1, 1};
+    double len[3] = {1, 1, 1};
+    int64_t plane = 0;                // points per plane of the slowest axis
+    int64_t nslow = 0;                // extent of the slowest axis
+    int64_t points = 0;
+    // scheme (ascending n_k)
+    std::vector<int> nk_all;
+    std::vector<double> wk_all;
+    std::vector<int> my_seq;          // indices into nk_all run by this rank
+    // distribution
+    int rank = 0, world = 1, device = 0, groups = 1, slabs = 1, my_group = 0, my_slab = 0;
+    int loopback = 1;                 // local slabs on this GPU
+    nccl::comm_t comm_world = nullptr, comm_slab = nullptr, comm_group = nullptr;
+    // memory
+    std::vector<Slab> slab;
+    int64_t ghost = 0;                // ghost planes per side (R when slabbed)
+    int64_t field_stride = 0;         // doubles per field incl. ghosts
+    int yb = 0;                       // which of buf[0]/buf[1] is Y
+    int* d_flag = nullptr;
+    double* d_gather = nullptr;       // multi-GPU read_state staging
+    // execution
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool have_state = false;
+    bool use_graph = true;
+    bool time_kernels = false;
+    bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
+    bool use_persistent = true;       // one cluster launch per gbs_advance for small 1-D grids
+    double* d_alpha = nullptr;        // spectral derivative weights (order 0)
+    // asynchronous slab IO (gbs_write_slab_async / gbs_read_slab_async): per local slab a
+    // staging buffer for the incoming and for the outgoing state, own copy streams
+    std::vector<double*> in_buf, out_buf;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr, ev_out_ready = nullptr, ev_out_free = nullptr;
+    bool pending_in = false;
+    // halo exchange overlapped with the interior planes (slabbed layouts)
+    bool use_overlap = true;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
+    double* d_wh = nullptr;
+    bool use_fuse = true;             // two-substep (temporally blocked) kernels where eligible
+                                      // (bit-exact)
+    bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
+    int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
+    int zchunk_opt = 0;
+    int sms = 148;                    // streaming multiprocessors of the device
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    double graph_H = -1.0;
+    int64_t macro_done = 0;
+    int64_t launches = 0;
+    int64_t launches_per_macro = 0;
+    double t = 0.0;
+    KernelTimer timer;
+    std::string err;
+};
+
+extern thread_local std::string g_err;
+int fail(gbs_ctx* c, int code, const char* fmt, ...);
+
+#define CU(c, call)                                                                      \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(c, GBS_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NC(c, call)                                                                         \
+    do {                                                                                    \
+        int r_ = (call);                                                                    \
+        if (r_ != nccl::ncclSuccess)                                                        \
+            return fail(c, GBS_E_NCCL, "%s failed: %s", #call, nccl::api().GetErrorString(r_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// memory helpers
+// ---------------------------------------------------------------------------
+inline double* field_ptr(gbs_ctx* c, Slab& s, int b, int f) {
+    return s.buf[b] + (int64_t)f * c->field_stride + c->ghost * c->plane;
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+// ---------------------------------------------------------------------------
+struct Slot { int b, f; };   // one field of one state buffer
+struct StepOperands {
+    int S, P, O;          // buffer indices of the current level, previous level, output
+    int mode;
+    double cf, wh;
+    bool flag;
+    Slot xu = {-1, 0};    // FE only (TMA kernel): also write u_2 = S_u + cf2 v_1 here
+    double cf2 = 0.0;
+};
+
+// Two consecutive substeps of one sequence in one launch (3-D wave, TMA grids),
+// gbs_wave3d_pair.cuh.  Operands are field slots (buffer, field): the pair
+// kernel reads P_v, S = (S_u, S_v) and U = u_{n+1}; LF writes Av = v_{n+1},
+// (Bu, Bv) = y_{n+2} and Cu = u_{n+3}; FIN0/FINACC writes the accumulator
+// buffer's two fields only.
+struct PairOperands {
+    Slot Pv, Su, Sv, U;
+    Slot Av, Bu, Bv, Cu;          // LF outputs (Bu.b = the accumulator buffer for FIN)
+    int modeB;
+    double cfA, cfB, wh;
+    bool flag;
+};
+
+// ---- gbs_plan.cu
+std::vector<std::vector<int>> partition(const std::vector<int>& nk, int g);
+int64_t crit_path(const std::vector<int>& nk, int g);
+void plan(gbs_ctx* c, int want_groups);
+std::vector<gbs_halo_op> halo_schedule(int slabs, int my_slab, int64_t nz, int G, unsigned mask);
+int validate(gbs_ctx* c, const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, const double* w_k);
+int make_plan(gbs_ctx* c, int rank, int world, int groups);
+// ---- gbs_launch.cu
+int alloc_state(gbs_ctx* c);
+void free_state(gbs_ctx* c);
+int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi);
+int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi);
+bool persistent_path(const gbs_ctx* c);
+int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);
+// ---- gbs_exec.cu
+int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev);
+int harvest_timer(gbs_ctx* c);
+// ---- gbs_io.cu
+void async_release(gbs_ctx* c);
+int consume_in(gbs_ctx* c);
+int check_flag(gbs_ctx* c);

@@ -1,0 +1,447 @@
+// gbs_launch.cu -- device memory (state buffers, ghost planes, tensor maps) and
+// every kernel launch: the per-substep kernels (register z/y-march, TMA-pipelined
+// 3-D and 2-D, the two-substep 3-D kernel) over a plane range of a slab, and the
+// whole-run thread-block-cluster kernel for small 1-D grids (FD and spectral).
+#include "gbs_internal.h"
+#include "gbs_kernels.cuh"
+#include "gbs_wave3d_tma.cuh"
+#include "gbs_wave3d_pair.cuh"
+#include "gbs_acoustic2d_tma.cuh"
+#include "gbs_adv1d_cluster.cuh"
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled_t encode_tiled() {
+    static EncodeTiled_t fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiled_t)p;
+    }
+    return fn;
+}
+
+// 3-D fp64 view [dz][ny][nx] at base with box (bx, by, 1)
+static bool make_map(CUtensorMap* m, double* base, int64_t nx, int64_t ny, int64_t dz, int bx, int by) {
+    EncodeTiled_t enc = encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)dz};
+    cuuint64_t strides[2] = {(cuuint64_t)nx * 8, (cuuint64_t)(nx * ny) * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int alloc_state(gbs_ctx* c) {
+    int nloc = c->loopback;
+    int64_t total_slabs = (int64_t)c->slabs * nloc;
+    int64_t nzl = c->nslow / total_slabs;
+    c->ghost = total_slabs > 1 ? c->R : 0;
+    c->field_stride = (nzl + 2 * c->ghost) * c->plane;
+    // the TMA (and two-substep) kernels need the grid to be a multiple of their tile so
+    // halo boxes never cross the wrap; the two-substep kernels need 4 level buffers
+    // (2-D acoustics: x a multiple of the tile width, each slab's rows a multiple of its height)
+    c->tma_grid = (c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0) ||
+                  (c->pde == GBS_ACOUSTIC2D && c->n[0] % gbs::tma::TX == 0 && nzl % gbs::tma::TY == 0);
+    c->nbuf = (c->tma_grid && c->pde == GBS_WAVE3D) ? 6 : 4;
+    c->slab.resize(nloc);
+    for (int v = 0; v < nloc; ++v) {
+        Slab& s = c->slab[v];
+        int64_t gidx = (int64_t)c->my_slab * nloc + v;
+        s.z0 = gidx * nzl;
+        s.nz = nzl;
+        for (int b = 0; b < c->nbuf; ++b) {
+            size_t bytes = sizeof(double) * (size_t)c->F * (size_t)c->field_stride;
+            if (cudaMalloc(&s.buf[b], bytes) != cudaSuccess)
+                return fail(c, GBS_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
+            CU(c, cudaMemsetAsync(s.buf[b], 0, bytes, c->stream));
+        }
+        // TMA kernels: the grid must be a multiple of the tile so halo boxes never cross the wrap
+        s.tma_ok = false;
+        if (c->tma_grid) {
+            bool ok = true;
+            const int64_t dz = nzl + 2 * c->ghost;
+            // 3-D: views [dz][ny][nx]; 2-D: [1][ny_alloc][nx] (the slow axis is y)
+            const int64_t vy = c->pde == GBS_WAVE3D ? c->n[1] : dz, vz = c->pde == GBS_WAVE3D ? dz : 1;
+            for (int b = 0; b < c->nbuf && ok; ++b)
+                for (int f = 0; f < c->F && ok; ++f) {
+                    double* base = s.buf[b] + (int64_t)f * c->field_stride;
+                    ok = make_map(&s.tm[b][f][0], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY) &&
+                         make_map(&s.tm[b][f][1], base, c->n[0], vy, vz, gbs::tma::TX, c->R) &&
+                         make_map(&s.tm[b][f][2], base, c->n[0], vy, vz, c->R, gbs::tma::TY);
+                }
+            s.tma_ok = ok;
+        }
+    }
+    CU(c, cudaMalloc(&c->d_flag, sizeof(int)));
+    CU(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    return GBS_OK;
+}
+
+void free_state(gbs_ctx* c) {
+    for (auto& s : c->slab)
+        for (int b = 0; b < 6; ++b)
+            if (s.buf[b]) { cudaFree(s.buf[b]); s.buf[b] = nullptr; }
+    c->slab.clear();
+}
+
+template <int R, int MODE, bool SLAB>
+static void launch_wave3d(const gbs::Wave3DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
+    if (vx2) gbs::wave3d_step<R, MODE, 2, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
+    else gbs::wave3d_step<R, MODE, 1, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
+}
+template <int R, int MODE, bool SLAB>
+static cudaError_t launch_wave3d_tma(const gbs::tma::Maps& m, const gbs::Wave3DArgs& a, int zbase, dim3 grid,
+                                     cudaStream_t st) {
+    using L = gbs::tma::Layout<R, MODE>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::wave3d_step_tma<R, MODE, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gbs::tma::wave3d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, zbase);
+    return cudaSuccess;
+}
+template <int R, int MODEB, bool SLAB>
+static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::PairArgs& a, int zbase, dim3 grid,
+                                   cudaStream_t st) {
+    using L = gbs::tma::PairLayout<R, MODEB>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::wave3d_pair_tma<R, MODEB, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY / 2), L::bytes, st>>>(m, a, zbase);
+    return cudaSuccess;
+}
+template <int R, int MODE, bool SLAB>
+static cudaError_t launch_ac2d_tma(const gbs::tma::AcMaps& m, const gbs::Acoustic2DArgs& a, int ybase, dim3 grid,
+                                   cudaStream_t st) {
+    using L = gbs::tma::AcLayout<R, MODE>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::acoustic2d_step_tma<R, MODE, SLAB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gbs::tma::acoustic2d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, ybase);
+    return cudaSuccess;
+}
+// rows per CTA of the 2-D TMA kernel: a multiple of the tile height minimising
+// (waves of one-CTA-per-SM) x (rows + ~2 tiles of pipeline fill)
+static int ac2d_ychunk(int64_t xtiles, int64_t ny, int opt, int sms) {
+    const int T = gbs::tma::TY;
+    if (opt > 0) return (int)std::min<int64_t>(ny, ((opt + T - 1) / T) * T);
+    int64_t best = -1, bestc = T;
+    for (int64_t yc = T; yc <= ny; yc += T) {
+        const int64_t ctas = xtiles * ((ny + yc - 1) / yc);
+        const int64_t cost = ((ctas + sms - 1) / sms) * (yc + 2 * T);
+        if (best < 0 || cost < best) { best = cost; bestc = yc; }
+    }
+    return (int)bestc;
+}
+template <int R, int MODE, bool SLAB>
+static void launch_ac2d(const gbs::Acoustic2DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
+    if (vx2) gbs::acoustic2d_step<R, MODE, 2, 128, SLAB><<<grid, 128, 0, st>>>(a);
+    else gbs::acoustic2d_step<R, MODE, 1, 128, SLAB><<<grid, 128, 0, st>>>(a);
+}
+
+static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
+    if (zchunk_opt > 0) return (int)std::min<int64_t>(zchunk_opt, extent);
+    // aim at >= ~16 resident waves of CTAs so the tail stays small, with
+    // chunks of at least 32 planes so the 2r warm-up planes stay cheap
+    const int64_t target = 148 * 2 * 16;
+    int64_t chunks = std::max<int64_t>(1, (target + tiles - 1) / tiles);
+    chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, extent / 32));
+    return (int)((extent + chunks - 1) / chunks);
+}
+
+// one substep over the planes [lo, hi) of slab s (lo = 0, hi = s.nz: the whole slab)
+int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi) {
+    const bool slab = c->ghost > 0;
+    int* flag = op.flag ? c->d_flag : nullptr;
+    if (c->pde == GBS_WAVE3D) {
+        gbs::Wave3DArgs a;
+        a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1);
+        a.Pu = field_ptr(c, s, op.P, 0); a.Pv = field_ptr(c, s, op.P, 1);
+        a.Ou = field_ptr(c, s, op.O, 0); a.Ov = field_ptr(c, s, op.O, 1);
+        a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
+        a.plane = c->plane;
+        const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
+        a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
+        a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        a.Xu = op.xu.b >= 0 ? field_ptr(c, s, op.xu.b, op.xu.f) : nullptr;
+        a.cf2 = op.cf2;
+        const bool vx2 = (c->n[0] % 2) == 0;
+        if (c->use_bulk && s.tma_ok) {
+            int64_t tx = c->n[0] / gbs::tma::TX, ty = c->n[1] / gbs::tma::TY;
+            a.zlo = (int)lo; a.zhi = (int)hi;
+            a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo)
+                                         : (int)std::min<int64_t>(128, hi - lo);
+            dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+            gbs::tma::Maps m;
+            m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
+            m.sv = s.tm[op.S][1][0];
+            m.pu = s.tm[op.P][0][0]; m.pv = s.tm[op.P][1][0];
+            m.au = s.tm[op.O][0][0]; m.av = s.tm[op.O][1][0];
+            const int zbase = (int)c->ghost;
+            cudaError_t e = cudaSuccess;
+#define W3B(RR, SL)                                                                                   \
+            switch (op.mode) {                                                                        \
+                case gbs::MODE_FE: e = launch_wave3d_tma<RR, gbs::MODE_FE, SL>(m, a, zbase, grid, c->stream); break;     \
+                case gbs::MODE_LF: e = launch_wave3d_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream); break;     \
+                case gbs::MODE_FIN0: e = launch_wave3d_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break; \
+                default: e = launch_wave3d_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;           \
+            }
+            if (c->R == 2) { if (slab) { W3B(2, true) } else { W3B(2, false) } }
+            else { if (slab) { W3B(4, true) } else { W3B(4, false) } }
+#undef W3B
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "bulk kernel setup: %s", cudaGetErrorString(e));
+            c->launches++;
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return GBS_OK;
+        }
+        const int TX = vx2 ? 64 : 32, TY = 16;
+        int64_t tx = (c->n[0] + TX - 1) / TX, ty = (c->n[1] + TY - 1) / TY;
+        a.zlo = (int)lo; a.zhi = (int)hi;
+        a.zchunk = chunk_for(tx * ty, hi - lo, c->zchunk_opt);
+        dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+#define W3(RR, SL)                                                                   \
+        switch (op.mode) {                                                           \
+            case gbs::MODE_FE: launch_wave3d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_LF: launch_wave3d<RR, gbs::MODE_LF, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_FIN0: launch_wave3d<RR, gbs::MODE_FIN0, SL>(a, grid, vx2, c->stream); break; \
+            default: launch_wave3d<RR, gbs::MODE_FINACC, SL>(a, grid, vx2, c->stream); break;         \
+        }
+        if (c->R == 2) { if (slab) { W3(2, true) } else { W3(2, false) } }
+        else { if (slab) { W3(4, true) } else { W3(4, false) } }
+#undef W3
+    } else if (c->pde == GBS_ACOUSTIC2D) {
+        gbs::Acoustic2DArgs a;
+        for (int f = 0; f < 3; ++f) {
+            a.S[f] = field_ptr(c, s, op.S, f);
+            a.P[f] = field_ptr(c, s, op.P, f);
+            a.O[f] = field_ptr(c, s, op.O, f);
+        }
+        a.nx = (int)c->n[0]; a.ny = (int)s.nz;
+        a.sx = c->n[0] / c->len[0]; a.sy = c->n[1] / c->len[1];
+        a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        if (c->use_bulk && s.tma_ok) {
+            const int64_t xt = c->n[0] / gbs::tma::TX;
+            a.ylo = (int)lo; a.yhi = (int)hi;
+            a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms);
+            dim3 grid((unsigned)xt, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
+            gbs::tma::AcMaps m;
+            for (int f = 0; f < 3; ++f) {
+                m.s_a[f] = s.tm[op.S][f][0]; m.s_b[f] = s.tm[op.S][f][1]; m.s_c[f] = s.tm[op.S][f][2];
+                m.p[f] = s.tm[op.P][f][0];
+                m.acc[f] = s.tm[op.O][f][0];
+            }
+            const int ybase = (int)c->ghost;
+            cudaError_t e = cudaSuccess;
+#define A2B(RR, SL)                                                                                     \
+            switch (op.mode) {                                                                          \
+                case gbs::MODE_FE: e = launch_ac2d_tma<RR, gbs::MODE_FE, SL>(m, a, ybase, grid, c->stream); break;     \
+                case gbs::MODE_LF: e = launch_ac2d_tma<RR, gbs::MODE_LF, SL>(m, a, ybase, grid, c->stream); break;     \
+                case gbs::MODE_FIN0: e = launch_ac2d_tma<RR, gbs::MODE_FIN0, SL>(m, a, ybase, grid, c->stream); break; \
+                default: e = launch_ac2d_tma<RR, gbs::MODE_FINACC, SL>(m, a, ybase, grid, c->stream); break;           \
+            }
+            if (c->R == 2) { if (slab) { A2B(2, true) } else { A2B(2, false) } }
+            else { if (slab) { A2B(4, true) } else { A2B(4, false) } }
+#undef A2B
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "bulk kernel setup: %s", cudaGetErrorString(e));
+            c->launches++;
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return GBS_OK;
+        }
+        const bool vx2 = (c->n[0] % 2) == 0;
+        const int TX = vx2 ? 256 : 128;
+        int64_t tx = (c->n[0] + TX - 1) / TX;
+        a.ylo = (int)lo; a.yhi = (int)hi;
+        a.ychunk = chunk_for(tx, hi - lo, c->zchunk_opt);
+        dim3 grid((unsigned)tx, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
+#define A2(RR, SL)                                                                   \
+        switch (op.mode) {                                                           \
+            case gbs::MODE_FE: launch_ac2d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_LF: launch_ac2d<RR, gbs::MODE_LF, SL>(a, grid, vx2, c->stream); break;   \
+            case gbs::MODE_FIN0: launch_ac2d<RR, gbs::MODE_FIN0, SL>(a, grid, vx2, c->stream); break; \
+            default: launch_ac2d<RR, gbs::MODE_FINACC, SL>(a, grid, vx2, c->stream); break;         \
+        }
+        if (c->R == 2) { if (slab) { A2(2, true) } else { A2(2, false) } }
+        else { if (slab) { A2(4, true) } else { A2(4, false) } }
+#undef A2
+    } else {
+        gbs::Adv1DArgs a;
+        a.S = field_ptr(c, s, op.S, 0); a.P = field_ptr(c, s, op.P, 0); a.O = field_ptr(c, s, op.O, 0);
+        a.nx = (int)c->n[0]; a.sx = c->n[0] / c->len[0];
+        a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        constexpr int NT = 256;
+        dim3 grid((unsigned)((c->n[0] + NT - 1) / NT));
+#define A1(RR)                                                                            \
+        switch (op.mode) {                                                                \
+            case gbs::MODE_FE: gbs::adv1d_step<RR, gbs::MODE_FE, NT><<<grid, NT, 0, c->stream>>>(a); break;   \
+            case gbs::MODE_LF: gbs::adv1d_step<RR, gbs::MODE_LF, NT><<<grid, NT, 0, c->stream>>>(a); break;   \
+            case gbs::MODE_FIN0: gbs::adv1d_step<RR, gbs::MODE_FIN0, NT><<<grid, NT, 0, c->stream>>>(a); break; \
+            default: gbs::adv1d_step<RR, gbs::MODE_FINACC, NT><<<grid, NT, 0, c->stream>>>(a); break;         \
+        }
+        if (c->R == 2) { A1(2) } else { A1(4) }
+#undef A1
+    }
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
+int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi) {
+    const bool slab = c->ghost > 0;
+    const bool lf = op.modeB == gbs::MODE_LF;
+    gbs::tma::PairArgs a;
+    if (lf) {
+        a.Av = field_ptr(c, s, op.Av.b, op.Av.f);
+        a.Bu = field_ptr(c, s, op.Bu.b, op.Bu.f); a.Bv = field_ptr(c, s, op.Bv.b, op.Bv.f);
+        a.Cu = field_ptr(c, s, op.Cu.b, op.Cu.f);
+    } else {
+        a.Av = a.Cu = nullptr;
+        a.Bu = field_ptr(c, s, op.Bu.b, 0); a.Bv = field_ptr(c, s, op.Bu.b, 1);
+    }
+    a.Su = field_ptr(c, s, op.Su.b, op.Su.f);
+    a.U = field_ptr(c, s, op.U.b, op.U.f);
+    a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
+    a.plane = c->plane;
+    const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
+    a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
+    a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
+    a.nonfinite = op.flag ? c->d_flag : nullptr;
+    a.zlo = (int)lo; a.zhi = (int)hi;
+    a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo) : (int)std::min<int64_t>(128, hi - lo);
+    dim3 grid((unsigned)(c->n[0] / gbs::tma::TX), (unsigned)(c->n[1] / gbs::tma::TY),
+              (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+    gbs::tma::PairMaps m;
+    m.su_a = s.tm[op.Su.b][op.Su.f][0]; m.su_b = s.tm[op.Su.b][op.Su.f][1]; m.su_c = s.tm[op.Su.b][op.Su.f][2];
+    m.u_a = s.tm[op.U.b][op.U.f][0]; m.u_b = s.tm[op.U.b][op.U.f][1]; m.u_c = s.tm[op.U.b][op.U.f][2];
+    m.sv = s.tm[op.Sv.b][op.Sv.f][0];
+    m.pv = s.tm[op.Pv.b][op.Pv.f][0];
+    m.acc_u = s.tm[op.Bu.b][0][0]; m.acc_v = s.tm[op.Bu.b][1][0];
+    const int zbase = (int)c->ghost;
+    cudaError_t e = cudaSuccess;
+#define PR(RR, SL)                                                                                          \
+    switch (op.modeB) {                                                                                     \
+        case gbs::MODE_LF: e = launch_pair_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream); break;     \
+        case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break; \
+        default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;           \
+    }
+    if (c->R == 2) { if (slab) { PR(2, true) } else { PR(2, false) } }
+    else { if (slab) { PR(4, true) } else { PR(4, false) } }
+#undef PR
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "pair kernel setup: %s", cudaGetErrorString(e));
+    c->launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// small 1-D grids: the whole run in one cluster launch (K6)
+// ---------------------------------------------------------------------------
+
+bool persistent_path(const gbs_ctx* c) {
+    const int m = (int)c->my_seq.size();
+    return c->use_persistent && c->pde == GBS_ADV1D && c->world == 1 && c->loopback == 1 && m >= 1 &&
+           m <= 16 && c->n[0] <= kClusterMaxN;
+}
+
+int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H) {
+    const int m = (int)c->my_seq.size();
+    if (!c->d_nk) {
+        std::vector<int> nk;
+        std::vector<double> wh;
+        for (int k : c->my_seq) { nk.push_back(c->nk_all[k]); wh.push_back(0.5 * c->wk_all[k]); }
+        CU(c, cudaMalloc(&c->d_nk, sizeof(int) * m));
+        CU(c, cudaMalloc(&c->d_wh, sizeof(double) * m));
+        CU(c, cudaMemcpyAsync(c->d_nk, nk.data(), sizeof(int) * m, cudaMemcpyHostToDevice, c->stream));
+        CU(c, cudaMemcpyAsync(c->d_wh, wh.data(), sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+    }
+    gbs::Adv1DClusterArgs a;
+    a.Y = field_ptr(c, c->slab[0], c->yb, 0);
+    a.nx = (int)c->n[0];
+    a.sx = c->n[0] / c->len[0];
+    a.H = H;
+    a.macro_steps = macro_steps;
+    a.nk = c->d_nk;
+    a.wh = c->d_wh;
+    a.nonfinite = c->d_flag;
+    const bool spectral = c->order == 0;
+    const size_t smem = sizeof(double) * (4 * (size_t)a.nx + (spectral ? (size_t)a.nx / 2 : 0));
+    if (spectral && !c->d_alpha) {
+        // alpha_j = pi (-1)^{j+1} cot(j pi / N) / N, j = 1 .. N/2 - 1 (gbs_adv1d_cluster.cuh)
+        const int64_t N = c->n[0];
+        std::vector<double> al((size_t)(N / 2 - 1));
+        for (int64_t j = 1; j <= N / 2 - 1; ++j)
+            al[(size_t)(j - 1)] = (j % 2 ? 1.0 : -1.0) * M_PI / std::tan((double)j * M_PI / (double)N) / (double)N;
+        CU(c, cudaMalloc(&c->d_alpha, sizeof(double) * al.size() + 8));
+        CU(c, cudaMemcpyAsync(c->d_alpha, al.data(), sizeof(double) * al.size(), cudaMemcpyHostToDevice,
+                              c->stream));
+    }
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (spectral) {
+        auto kern = gbs::adv1d_cluster_run_spectral;
+        CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (m > 8) CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)m);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)m;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const double* alpha = c->d_alpha;
+        if (c->time_kernels && (rc = timed_begin(c, 5, &end))) return rc;
+        CU(c, cudaLaunchKernelEx(&cfg, kern, a, alpha));
+        if (end) CU(c, cudaEventRecord(end, c->stream));
+        c->launches++;
+        return GBS_OK;
+    }
+    void (*kern)(const gbs::Adv1DClusterArgs) =
+        c->R == 2 ? gbs::adv1d_cluster_run<2> : gbs::adv1d_cluster_run<4>;
+    CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (m > 8) CU(c, cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)m);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)m;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (c->time_kernels && (rc = timed_begin(c, 5, &end))) return rc;
+    CU(c, cudaLaunchKernelEx(&cfg, kern, a));
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    c->launches++;
+    return GBS_OK;
+}
