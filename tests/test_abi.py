@@ -68,6 +68,19 @@ def test_create_without_gpu_fails_loudly(lib):
     assert e.value.code == gbs.GBS_E_CUDA
 
 
+def test_null_context_calls_fail_cleanly(lib):
+    """Every entry point taking a context rejects NULL with GBS_E_INVAL (no crash, no GPU)."""
+    import ctypes
+    L = gbs.load()
+    buf = (ctypes.c_double * 4)()
+    for fn in ("gbs_write_state", "gbs_read_state", "gbs_write_slab", "gbs_read_slab",
+               "gbs_write_slab_async", "gbs_read_slab_async"):
+        assert getattr(L, fn)(None, ctypes.cast(buf, ctypes.c_void_p), 4, 0) == gbs.GBS_E_INVAL, fn
+    assert L.gbs_advance(None, 1, 1e-3) == gbs.GBS_E_INVAL
+    assert L.gbs_sync(None) == gbs.GBS_E_INVAL
+    L.gbs_destroy(None)                     # no-op
+
+
 def test_argument_validation_precedes_device(lib):
     """Invalid arguments are rejected with the documented codes even without a GPU."""
     cases = [
