@@ -217,7 +217,9 @@ def run_ours(a):
         return pdist.max_over_ranks(x, dev)
 
     with torch.cuda.stream(stream):
-        st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream)
+        # the state buffers live in a torch tensor (gbs_bind_workspace): PyTorch owns device memory
+        st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream,
+                         torch_memory=True)
         y0_dev = torch.from_numpy(y0).to("cuda", non_blocking=False)
         st.write_slab(y0_dev)
         gbs.gbs_sync(st.ctx)

@@ -189,6 +189,18 @@ GBS_API int gbs_read_state(gbs_ctx* ctx, double* dst, int64_t count, int on_devi
 GBS_API int gbs_write_slab(gbs_ctx* ctx, const double* src, int64_t count, int on_device);
 GBS_API int gbs_read_slab(gbs_ctx* ctx, double* dst, int64_t count, int on_device);
 
+/* Device memory.  The state buffers (F x points x 8 bytes each, 4 or 6 of them per local
+ * slab incl. ghost planes) are allocated on the first write, by the context (cudaMalloc), or
+ * carved out of a caller-owned workspace bound before that -- e.g. a torch tensor, so that
+ * PyTorch's allocator owns the memory:
+ *   gbs_workspace_bytes  bytes the current layout needs (depends on options such as loopback)
+ *   gbs_bind_workspace   device_ptr (256-byte aligned, >= gbs_workspace_bytes) replaces the
+ *                        context's own buffers (released); NULL returns to own buffers.  The
+ *                        state is discarded: write it again.  The caller keeps the memory
+ *                        alive and untouched until gbs_destroy or the next bind. */
+GBS_API int gbs_workspace_bytes(const gbs_ctx* ctx, int64_t* bytes);
+GBS_API int gbs_bind_workspace(gbs_ctx* ctx, void* device_ptr, int64_t bytes);
+
 /* Asynchronous slab IO (same layout and count as gbs_write_slab / gbs_read_slab; on one
  * GPU the slab is the whole grid).  The copies run on the context's own copy streams and
  * overlap the macro steps queued on the context stream:

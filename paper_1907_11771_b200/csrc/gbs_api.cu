@@ -192,6 +192,32 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     return fail(c, GBS_E_INVAL, "unknown option '%s'", key);
 }
 
+int gbs_workspace_bytes(const gbs_ctx* c, int64_t* bytes) {
+    if (!c || !bytes) return fail(const_cast<gbs_ctx*>(c), GBS_E_INVAL, "ctx or bytes is NULL");
+    *bytes = state_bytes(c);
+    return GBS_OK;
+}
+
+int gbs_bind_workspace(gbs_ctx* c, void* device_ptr, int64_t bytes) {
+    if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    if (device_ptr && bytes < state_bytes(c))
+        return fail(c, GBS_E_INVAL, "workspace of %lld bytes < %lld (gbs_workspace_bytes)", (long long)bytes,
+                    (long long)state_bytes(c));
+    if (device_ptr && (reinterpret_cast<uintptr_t>(device_ptr) % 256))
+        return fail(c, GBS_E_INVAL, "workspace must be 256-byte aligned");
+    CU(c, cudaSetDevice(c->device));
+    CU(c, cudaStreamSynchronize(c->stream));
+    int rc = consume_in(c);
+    if (rc) return rc;
+    CU(c, cudaStreamSynchronize(c->stream));
+    for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    free_state(c);                      // own buffers are released; a workspace is only forgotten
+    c->ws_ptr = device_ptr;
+    c->ws_bytes = device_ptr ? bytes : 0;
+    c->have_state = false;              // the state must be written again
+    return GBS_OK;
+}
+
 int gbs_query(const gbs_ctx* c, gbs_info* info) {
     if (!c || !info) return fail(const_cast<gbs_ctx*>(c), GBS_E_INVAL, "ctx or info is NULL");
     memset(info, 0, sizeof(*info));

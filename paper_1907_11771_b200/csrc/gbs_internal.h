@@ -109,6 +109,10 @@ struct gbs_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in_ready = nullptr, ev_in_free = nullptr, ev_out_ready = nullptr, ev_out_free = nullptr;
     bool pending_in = false;
+    // state buffers: carved from a caller-bound workspace (gbs_bind_workspace) or owned
+    bool buffers_ready = false;
+    void* ws_ptr = nullptr;
+    int64_t ws_bytes = 0;
     // halo exchange overlapped with the interior planes (slabbed layouts)
     bool use_overlap = true;
     cudaStream_t cstream = nullptr;
@@ -189,7 +193,9 @@ std::vector<gbs_halo_op> halo_schedule(int slabs, int my_slab, int64_t nz, int G
 int validate(gbs_ctx* c, const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, const double* w_k);
 int make_plan(gbs_ctx* c, int rank, int world, int groups);
 // ---- gbs_launch.cu
-int alloc_state(gbs_ctx* c);
+int alloc_state(gbs_ctx* c);            // layout + flag; buffers on first use
+int ensure_buffers(gbs_ctx* c);         // allocate (or carve) the state buffers, tensor maps
+int64_t state_bytes(const gbs_ctx* c);  // device bytes of the state buffers of this layout
 void free_state(gbs_ctx* c);
 int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi);
 int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi);

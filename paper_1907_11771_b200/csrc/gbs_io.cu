@@ -87,6 +87,7 @@ int gbs_write_state(gbs_ctx* c, const double* src, int64_t count, int on_device)
         return fail(c, GBS_E_INVAL, "count=%lld, expected F*points=%lld", (long long)count, (long long)(c->F * c->points));
     CU(c, cudaSetDevice(c->device));
     int rc0 = consume_in(c);
+    if (!rc0) rc0 = ensure_buffers(c);
     if (rc0) return rc0;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     for (auto& s : c->slab)
@@ -149,6 +150,7 @@ int gbs_write_slab(gbs_ctx* c, const double* src, int64_t count, int on_device) 
                     (long long)(c->F * per_field));
     CU(c, cudaSetDevice(c->device));
     int rc0 = consume_in(c);
+    if (!rc0) rc0 = ensure_buffers(c);
     if (rc0) return rc0;
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     for (auto& s : c->slab)
@@ -191,6 +193,7 @@ int gbs_write_slab_async(gbs_ctx* c, const double* src, int64_t count, int on_de
                     (long long)(c->F * per_field));
     CU(c, cudaSetDevice(c->device));
     int rc;
+    if ((rc = ensure_buffers(c))) return rc;
     if ((rc = async_setup(c))) return rc;
     if ((rc = consume_in(c))) return rc;            // an earlier staged state lands first
     CU(c, cudaStreamWaitEvent(c->h2d, c->ev_in_free, 0));

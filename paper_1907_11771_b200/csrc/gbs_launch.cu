@@ -40,6 +40,9 @@ static bool make_map(CUtensorMap* m, double* base, int64_t nx, int64_t ny, int64
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Layout of the state: slabs of the slowest axis with ghost planes, the number of
+// buffers per slab; no device memory yet (ensure_buffers allocates on first use, from
+// a caller-bound workspace when there is one).
 int alloc_state(gbs_ctx* c) {
     int nloc = c->loopback;
     int64_t total_slabs = (int64_t)c->slabs * nloc;
@@ -52,17 +55,46 @@ int alloc_state(gbs_ctx* c) {
     c->tma_grid = (c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0) ||
                   (c->pde == GBS_ACOUSTIC2D && c->n[0] % gbs::tma::TX == 0 && nzl % gbs::tma::TY == 0);
     c->nbuf = (c->tma_grid && c->pde == GBS_WAVE3D) ? 6 : 4;
-    c->slab.resize(nloc);
+    c->slab.assign(nloc, Slab());
     for (int v = 0; v < nloc; ++v) {
         Slab& s = c->slab[v];
         int64_t gidx = (int64_t)c->my_slab * nloc + v;
         s.z0 = gidx * nzl;
         s.nz = nzl;
+    }
+    c->buffers_ready = false;
+    if (!c->d_flag) {
+        CU(c, cudaMalloc(&c->d_flag, sizeof(int)));
+        CU(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    }
+    return GBS_OK;
+}
+
+static int64_t buffer_bytes(const gbs_ctx* c) {
+    const int64_t b = (int64_t)sizeof(double) * c->F * c->field_stride;
+    return (b + 255) / 256 * 256;                        // 256-byte aligned carve-out
+}
+
+int64_t state_bytes(const gbs_ctx* c) { return (int64_t)c->slab.size() * c->nbuf * buffer_bytes(c); }
+
+int ensure_buffers(gbs_ctx* c) {
+    if (c->buffers_ready) return GBS_OK;
+    const int64_t bb = buffer_bytes(c);
+    if (c->ws_ptr && c->ws_bytes < state_bytes(c))
+        return fail(c, GBS_E_INVAL, "bound workspace of %lld bytes < %lld needed by this layout",
+                    (long long)c->ws_bytes, (long long)state_bytes(c));
+    char* ws = static_cast<char*>(c->ws_ptr);
+    for (size_t v = 0; v < c->slab.size(); ++v) {
+        Slab& s = c->slab[v];
+        const int64_t nzl = s.nz;
         for (int b = 0; b < c->nbuf; ++b) {
-            size_t bytes = sizeof(double) * (size_t)c->F * (size_t)c->field_stride;
-            if (cudaMalloc(&s.buf[b], bytes) != cudaSuccess)
-                return fail(c, GBS_E_NOMEM, "cudaMalloc of %zu bytes failed", bytes);
-            CU(c, cudaMemsetAsync(s.buf[b], 0, bytes, c->stream));
+            if (ws) {
+                s.buf[b] = reinterpret_cast<double*>(ws + (int64_t)(v * c->nbuf + b) * bb);
+            } else if (cudaMalloc(&s.buf[b], (size_t)bb) != cudaSuccess) {
+                s.buf[b] = nullptr;
+                return fail(c, GBS_E_NOMEM, "cudaMalloc of %lld bytes failed", (long long)bb);
+            }
+            CU(c, cudaMemsetAsync(s.buf[b], 0, (size_t)bb, c->stream));
         }
         // TMA kernels: the grid must be a multiple of the tile so halo boxes never cross the wrap
         s.tma_ok = false;
@@ -81,16 +113,17 @@ int alloc_state(gbs_ctx* c) {
             s.tma_ok = ok;
         }
     }
-    CU(c, cudaMalloc(&c->d_flag, sizeof(int)));
-    CU(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    c->buffers_ready = true;
     return GBS_OK;
 }
 
 void free_state(gbs_ctx* c) {
     for (auto& s : c->slab)
-        for (int b = 0; b < 6; ++b)
-            if (s.buf[b]) { cudaFree(s.buf[b]); s.buf[b] = nullptr; }
-    c->slab.clear();
+        for (int b = 0; b < 6; ++b) {
+            if (s.buf[b] && !c->ws_ptr) cudaFree(s.buf[b]);
+            s.buf[b] = nullptr;
+        }
+    c->buffers_ready = false;
 }
 
 template <int R, int MODE, bool SLAB>

@@ -26,7 +26,8 @@ FIELDS = {"adv1d": 1, "acoustic2d": 3, "wave3d": 2}
 NDIM = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
 
 EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_write_slab",
-           "gbs_read_slab", "gbs_write_slab_async", "gbs_read_slab_async", "gbs_sync",
+           "gbs_read_slab", "gbs_write_slab_async", "gbs_read_slab_async", "gbs_workspace_bytes",
+           "gbs_bind_workspace", "gbs_sync",
            "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
            "gbs_set_option",
            "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
@@ -111,6 +112,8 @@ def load(build_if_missing: bool = False):
     L.gbs_read_slab.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_write_slab_async.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_read_slab_async.argtypes = [vp, vp, i64, ctypes.c_int]
+    L.gbs_workspace_bytes.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+    L.gbs_bind_workspace.argtypes = [vp, vp, i64]
     L.gbs_sync.argtypes = [vp]
     L.gbs_destroy.argtypes = [vp]
     L.gbs_destroy.restype = None
@@ -252,6 +255,23 @@ def gbs_read_slab_async(ctx, dst) -> None:
     _check(load().gbs_read_slab_async(ctx, ctypes.c_void_p(p), cnt, dev), ctx)
 
 
+def gbs_workspace_bytes(ctx) -> int:
+    b = ctypes.c_int64(0)
+    _check(load().gbs_workspace_bytes(ctx, ctypes.byref(b)), ctx)
+    return b.value
+
+
+def gbs_bind_workspace(ctx, ws) -> None:
+    """Bind a caller-owned device buffer (a torch tensor, or None to unbind) as the state memory."""
+    if ws is None:
+        _check(load().gbs_bind_workspace(ctx, None, 0), ctx)
+        return
+    import torch
+    if not (isinstance(ws, torch.Tensor) and ws.is_cuda and ws.is_contiguous()):
+        raise TypeError("workspace must be a contiguous CUDA tensor")
+    _check(load().gbs_bind_workspace(ctx, ctypes.c_void_p(ws.data_ptr()), ws.numel() * ws.element_size()), ctx)
+
+
 def gbs_sync(ctx) -> None:
     _check(load().gbs_sync(ctx), ctx)
 
@@ -289,11 +309,18 @@ def gbs_last_error(ctx=None) -> str:
 class Stepper:
     """RAII convenience around one context (still only marshalling)."""
 
-    def __init__(self, pde, n, stencil_order, n_k, w_k, dist=None, stream=None, **opts):
+    def __init__(self, pde, n, stencil_order, n_k, w_k, dist=None, stream=None, torch_memory=False, **opts):
         self.pde = pde
         self.ctx = gbs_create(pde, n, stencil_order, n_k, w_k, dist, stream)
         for k, v in opts.items():
             gbs_set_option(self.ctx, k, v)
+        self.workspace = None
+        if torch_memory:
+            # the state buffers live in a torch tensor (PyTorch's allocator owns the memory)
+            import torch
+            nbytes = gbs_workspace_bytes(self.ctx)
+            self.workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+            gbs_bind_workspace(self.ctx, self.workspace)
 
     def write(self, y):
         gbs_write_state(self.ctx, y)
@@ -329,6 +356,7 @@ class Stepper:
         if self.ctx:
             gbs_destroy(self.ctx)
             self.ctx = None
+        self.workspace = None
 
     def __enter__(self):
         return self

@@ -336,6 +336,37 @@ def test_async_io_pipeline(torch_cuda, cfg, n, lb):
                 assert np.array_equal(o.cpu().numpy(), r)
 
 
+@pytest.mark.parametrize("cfg,n,lb", [("c4", (64, 32, 24), 1), ("c5", (64, 48, 40), 2), ("c3", (128, 64, 1), 1),
+                                      ("c2", (200, 136, 1), 2)])
+def test_torch_owned_workspace(torch_cuda, cfg, n, lb):
+    """State buffers carved from a torch tensor (gbs_bind_workspace): same bytes as the
+    context's own allocation; the tensor really is the state memory (the bytes grow by
+    exactly gbs_workspace_bytes), and rebinding discards the state."""
+    gbs = gbs_mod()
+    torch = torch_cuda
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, _ = run_gpu(torch, w, counts, wd, H, 2, opts={"loopback": lb})
+    y0 = make_ic(w)
+    before = torch.cuda.memory_allocated()
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd, torch_memory=True, loopback=lb) as st:
+        nbytes = gbs.gbs_workspace_bytes(st.ctx)
+        assert torch.cuda.memory_allocated() - before >= nbytes > 0
+        st.write(y0)
+        st.advance(2, H)
+        out = np.empty_like(y0)
+        st.read(out)
+        assert np.array_equal(out, a[0])
+        gbs.gbs_bind_workspace(st.ctx, None)           # back to own buffers: state discarded
+        with pytest.raises(gbs.GbsError) as e:
+            st.advance(1, H)
+        assert e.value.code == gbs.GBS_E_STATE
+        small = torch.empty(16, dtype=torch.uint8, device="cuda")
+        with pytest.raises(gbs.GbsError) as e:
+            gbs.gbs_bind_workspace(st.ctx, small)
+        assert e.value.code == gbs.GBS_E_INVAL
+
+
 def test_graph_replay_is_bitwise_identical(torch_cuda):
     w = reduced("c4", (40, 36, 34), macro_steps=3, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8")
