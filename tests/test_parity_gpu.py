@@ -503,6 +503,27 @@ def test_2d_full_size_whole_run(torch_cuda, cfg):
 
 
 @pytest.mark.slow
+def test_c4_full_size_whole_run(torch_cuda):
+    """The whole BASELINE.json C4 run (512^3, FD8, {2..12}, 10 macro steps; the two-substep
+    TMA path) against the oracle over the full state after 5 and 10 macro steps (the oracle
+    takes about two minutes on the GPU box's host cores)."""
+    w = get_config("c4")
+    counts, wd, H = scheme_for(w)
+    gbs = gbs_mod()
+    torch = torch_cuda
+    y0 = make_ic(w)
+    ref = y0
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch.from_numpy(y0).cuda())
+        for done in (5, 10):
+            st.advance(5, H)
+            out = np.empty_like(y0)
+            st.read(out)
+            ref = C.advance(w.pde, w.order, ref, counts, wd, H, 5)
+            assert_parity(out, ref, what=f"c4 full, macro step {done}")
+
+
+@pytest.mark.slow
 def test_c5_whole_run_conserves_means(torch_cuda):
     """Property at full size: the whole C5 run (1024^3, 4 macro steps). The zero Fourier mode
     of the 3-D wave evolves as u0' = v0, v0' = 0 with R(0)=1, R'(0)=sum w = 1, so the means of
