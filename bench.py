@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--groups", type=int, default=0, help="sequence groups (0 = planner)")
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="library option (gbs_set_option) for this run, e.g. pdl=0")
     ap.add_argument("--weights", default=None,
                     help="weight set instead of the config's (e.g. opt8: the Appendix-B optimised "
                          "weights on the config's step counts; H follows their ISB)")
@@ -221,8 +223,9 @@ def run_ours(a):
 
     with torch.cuda.stream(stream):
         # the state buffers live in a torch tensor (gbs_bind_workspace): PyTorch owns device memory
+        opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
         st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream,
-                         torch_memory=True)
+                         torch_memory=True, **opts)
         y0_dev = torch.from_numpy(y0).to("cuda", non_blocking=False)
         st.write_slab(y0_dev)
         gbs.gbs_sync(st.ctx)
@@ -378,6 +381,7 @@ def run_ours(a):
                 "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": describe(w, H), "grid": list(w.n[: w.ndim]), "fields": F,
+                           "options": {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt},
                            "substeps_per_step": S, "step": "1 macro step (all sequences + combine)",
                            "l2": ("L2 flushed (512 MiB write) before every timed macro step: working set "
                                   "%.0f MiB < 2 x L2" % (6 * y0.nbytes / 2 ** 20) if flush else
