@@ -29,7 +29,6 @@ if a.fuse >= 0: gbs.gbs_set_option(st.ctx, "fuse", a.fuse)
 for kv in a.opt:
     k, v = kv.split("="); gbs.gbs_set_option(st.ctx, k, int(v))
 res_opts = dict(kv.split("=") for kv in a.opt)
-if os.environ.get("GBS_PAD"): res_opts["GBS_PAD"] = os.environ["GBS_PAD"]
 st.write(y0)
 st.advance(1, H); gbs.gbs_sync(st.ctx)
 gbs.gbs_set_option(st.ctx, "time_kernels", 1)
