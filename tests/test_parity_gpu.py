@@ -193,7 +193,11 @@ def test_reduced_every_macro_step(torch_cuda, cfg, n, M, wset):
 
 # ----------------------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("cfg,n,order", [("c4", (9, 9, 9), 8), ("c2", (5, 5, 1), 4),
-                                         ("c3", (9, 9, 1), 8), ("c1", (5, 1, 1), 4)])
+                                         ("c3", (9, 9, 1), 8), ("c1", (5, 1, 1), 4),
+                                         ("c4", (64, 16, 9), 8),     # two-substep TMA path, nz = 2r+1
+                                         ("c4", (64, 16, 5), 4),     # FD4 two-substep path, nz = 2r+1
+                                         ("c3", (64, 16, 1), 8),     # 2-D TMA path, one 16-row band
+                                         ("c2", (64, 16, 1), 4)])
 def test_minimum_grid(torch_cuda, cfg, n, order):
     w = reduced(cfg, n, macro_steps=2).with_(order=order)
     counts, wd, H = scheme_for(w)
@@ -377,7 +381,8 @@ def test_graph_replay_is_bitwise_identical(torch_cuda):
     assert ia["kernel_launches"] == ib["kernel_launches"] == 3 * 48
 
 
-@pytest.mark.parametrize("cfg,n,slabs", [("c4", (40, 36, 32), 2), ("c4", (40, 36, 32), 4),
+@pytest.mark.parametrize("cfg,n,slabs", [("c4", (64, 16, 16), 4),      # slabs exactly r planes thick
+                                         ("c4", (40, 36, 32), 2), ("c4", (40, 36, 32), 4),
                                          ("c4", (128, 32, 36), 3), ("c5", (64, 32, 32), 4),
                                          ("c5", (36, 20, 24), 3), ("c2", (96, 64, 1), 4),
                                          ("c3", (80, 48, 1), 3), ("c2", (128, 64, 1), 4),
