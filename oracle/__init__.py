@@ -14,7 +14,8 @@ each side derives independently from exact rationals.
 
 Modules
   gbs_oracle.c  fp64 stepping (FE, LF, averaging, weighted sum) on the MOL FD
-                right-hand sides; built into _build/liboracle_gbs.so
+                right-hand sides and the 1-D spectral derivative (a plain O(N^2)
+                DFT); built into _build/liboracle_gbs.so
   c_oracle      ctypes wrapper of the C library
   weights       exact-rational extrapolation weights (Eq. 3, 5, 6)
   stability     exact GBS stability polynomials, R(iy) scan, ISB, rho, H rule
@@ -24,5 +25,9 @@ Modules
 
 Parity status: every function above is pinned (see DESIGN.md "Oracle pins");
 none is "parity unpinned" except the choice of ICs and of the all-nonzero
-parity weight set, which the paper does not fix.
+parity weight set, which the paper does not fix.  The
+Appendix-B optimised free weights (gbs_inputs/optimized_schemes.json, weight
+set "opt8") are inputs written by the product's optimiser; the oracle checks
+them independently (exact order 8, its own ISB scan) and computes their
+dependent weights itself.
 """
