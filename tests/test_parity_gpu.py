@@ -273,6 +273,21 @@ def test_paper_scheme_gbs86(torch_cuda):
     assert info["substeps_per_macro"] == sum(n + 1 for n in counts)
 
 
+@pytest.mark.parametrize("wset", ["GBS_8_6", "GBS_8_8", "GBS_12_8", "FD12"])
+def test_paper_schemes_on_the_two_substep_path(torch_cuda, wset):
+    """The paper's printed schemes (§3.3, §3.8: 6-15 sequences, n_k up to 30, order
+    8 and 12) through the default 3-D path (TMA grid: FE + two-substep launches), against the
+    oracle, at each scheme's own H = 0.5 ISB / rho."""
+    counts, ws, _ = W.scheme(wset)
+    wd = W.to_double(ws)
+    w = reduced("c4", (64, 32, 24), macro_steps=2).with_(steps=tuple(counts), weights=wset)
+    H = S.macro_step_H(w.pde, w.order, w.n, counts, wd)
+    y0, g, info = run_gpu(torch_cuda, w, counts, wd, H, 2)
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(g[0], o[0], what=wset)
+    assert info["kernel_launches"] == 2 * sum(1 + n // 2 for n in counts)
+
+
 def test_host_buffers_match_device_buffers(torch_cuda):
     w = reduced("c2", (96, 64, 1), macro_steps=2, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8")
