@@ -23,6 +23,10 @@ static int async_setup(gbs_ctx* c) {
         double *in = nullptr, *out = nullptr;
         if (cudaMalloc(&in, bytes) != cudaSuccess || cudaMalloc(&out, bytes) != cudaSuccess) {
             if (in) cudaFree(in);
+            for (double* p : c->in_buf) cudaFree(p);          // all slabs or none
+            for (double* p : c->out_buf) cudaFree(p);
+            c->in_buf.clear();
+            c->out_buf.clear();
             return fail(c, GBS_E_NOMEM, "cudaMalloc of 2 x %zu bytes (async IO staging) failed", bytes);
         }
         c->in_buf.push_back(in);

@@ -92,6 +92,7 @@ int ensure_buffers(gbs_ctx* c) {
                 s.buf[b] = reinterpret_cast<double*>(ws + (int64_t)(v * c->nbuf + b) * bb);
             } else if (cudaMalloc(&s.buf[b], (size_t)bb) != cudaSuccess) {
                 s.buf[b] = nullptr;
+                free_state(c);                                // all buffers or none
                 return fail(c, GBS_E_NOMEM, "cudaMalloc of %lld bytes failed", (long long)bb);
             }
             CU(c, cudaMemsetAsync(s.buf[b], 0, (size_t)bb, c->stream));
