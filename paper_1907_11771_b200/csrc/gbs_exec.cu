@@ -32,7 +32,6 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st =
         fields = {0, 2};                        // acoustics: p and v cross the y slabs
     }
     const int nloc = c->loopback;
-    const int S = c->slabs * nloc;              // global slab count
     if (c->slabs == 1) {
         // all slabs local: device-to-device copies
         for (int v = 0; v < nloc; ++v) {
@@ -52,8 +51,6 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st =
         return GBS_OK;
     }
     if (nloc != 1) return fail(c, GBS_E_UNSUPPORTED, "loopback slabs with multi-GPU slabs");
-    (void)S;
-    (void)cnt;
     auto& A = nccl::api();
     Slab& me = c->slab[0];
     unsigned fm = 0;
