@@ -236,7 +236,10 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        halo copies through the multi-GPU code path (tests)
  *   "bulk"         1/0   TMA-pipelined 3-D kernels on grids that are multiples of
  *                        their 64 x 16 tile (default 1; 0 = register-prefetch kernels)
- *   "fuse"         1/0   two substeps per HBM pass on TMA grids (default 1)
+ *   "fuse"         1/0   two substeps per HBM pass on 3-D TMA grids (default 1)
+ *   "fuse2d"       1/0   2-D acoustics: two substeps per pass as the chain-U / chain-P
+ *                        kernel pair (default 0: bit-identical but measured slower
+ *                        than single substeps on B200)
  *   "persistent"   1/0   1-D grids up to 7000 points with m <= 16: every macro step of
  *                        a gbs_advance in one thread-block-cluster launch (default 1)
  *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)

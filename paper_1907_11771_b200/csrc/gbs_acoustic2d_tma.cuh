@@ -72,7 +72,7 @@ acoustic2d_step_tma(const __grid_constant__ AcMaps M, const Acoustic2DArgs A, co
     const int niter = (min(A.ychunk, A.yhi - ys) + TY - 1) / TY;   // ylo, ychunk, yhi: multiples of TY
     auto yc = [&](int y) -> int {              // tensor y coordinate of logical row y
         if constexpr (SLAB) return y + ybase;
-        else return wrap_any(y, ny);
+        else return wrap_any(y, ny) + ybase;    // ybase: ghost rows of the layout (0 on plain grids)
     };
 
     if (ty == 0 && lane == 0) {

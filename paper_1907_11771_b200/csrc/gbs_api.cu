@@ -169,9 +169,13 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "graph") { c->use_graph = value != 0 && c->world == 1; drop_graphs(); return GBS_OK; }
     if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "overlap") { c->use_overlap = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "l2hint") { c->hint_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "l2hint_step") { c->hint_step_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "band") { c->band_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "zchunk") { c->zchunk_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "fuse2d") { c->use_fuse2d = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "persistent") { c->use_persistent = value != 0; return GBS_OK; }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");

@@ -97,7 +97,7 @@ static int64_t face_band(const gbs_ctx* c, const Slab& s) {
 }
 
 static bool overlap_halo(gbs_ctx* c) {
-    if (c->ghost == 0 || !c->use_overlap) return false;
+    if (c->ghost == 0 || !c->use_overlap || c->slabs * c->loopback == 1) return false;
     for (const auto& s : c->slab)
         if (s.nz < 3 * face_band(c, s)) return false;
     return true;
@@ -121,8 +121,15 @@ static int comm_join(gbs_ctx* c) {
 }
 
 template <typename Launch>
-static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pair<int, unsigned>>& halos) {
+static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pair<int, unsigned>>& halos,
+                          bool self_ghosts = false) {
     int rc;
+    if (c->ghost > 0 && c->slabs * c->loopback == 1) {
+        // one slab with ghost rows (2-D TMA grids): only launches that read beyond the
+        // slab (self_ghosts) need them, refreshed by one copy kernel; the rest wrap
+        if (self_ghosts && (rc = launch_ghost_fill(c, halos))) return rc;
+        return launch(c->slab[0], (int64_t)0, c->slab[0].nz);
+    }
     if (!overlap_halo(c)) {
         for (auto& h : halos)
             if ((rc = exchange_halo(c, h.first, h.second))) return rc;
@@ -169,6 +176,20 @@ static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
     return GBS_OK;
 }
 
+// 2-D acoustics: two leap-frog substeps per pass (two chain kernels); they read S (p, u, v)
+// and P (p, v) with y stencils
+static int ac2d_pair_step(gbs_ctx* c, int cls, int P, int S, int Aout, int Bout, double cfA, double cfB) {
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
+    rc = run_overlapped(
+        c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_ac2d_pair(c, s, P, S, Aout, Bout, cfA, cfB, lo, hi); },
+        {{S, 0x7u}, {P, 0x5u}}, true);
+    if (rc) return rc;
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    return GBS_OK;
+}
+
 static bool fused_path(const gbs_ctx* c) {
     if (!(c->use_fuse && c->use_bulk && c->nbuf == 6)) return false;
     for (const auto& s : c->slab)
@@ -199,12 +220,29 @@ static int enqueue_macro(gbs_ctx* c, double H) {
     const int64_t l0 = c->launches;
     int rc;
     bool first = true;
-    const bool fused = fused_path(c);
+    const bool fused = fused_path(c) && c->pde == GBS_WAVE3D;
+    const bool fused2d = fused_path(c) && c->use_fuse2d && c->pde == GBS_ACOUSTIC2D;
     for (size_t q = 0; q < c->my_seq.size(); ++q) {
         const int k = c->my_seq[q];
         const int n = c->nk_all[k];
         const double h = H / (double)n;
         const bool last = (q + 1 == c->my_seq.size());
+        if (fused2d) {
+            // FE and LF1 single, then (LF2, LF3), ..., (LF_{n-2}, LF_{n-1}) two per pass
+            // (buffers (2,3) -> (4,5) -> (2,3) ...), then the final step single
+            if ((rc = step(c, 1, {Y, Y, 2, gbs::MODE_FE, h, 0.0, false}))) return rc;        // y1
+            if ((rc = step(c, 0, {2, Y, 3, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;  // y2
+            int P = 2, S = 3;
+            for (int p = 0; p < (n - 2) / 2; ++p) {
+                const int A = P == 2 ? 4 : 2, B = A + 1;
+                if ((rc = ac2d_pair_step(c, 3, P, S, A, B, 2.0 * h, 2.0 * h))) return rc;
+                P = A; S = B;
+            }
+            StepOperands fin{S, P, ACC, first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, h, 0.5 * c->wk_all[k], last};
+            if ((rc = step(c, 2, fin))) return rc;
+            first = false;
+            continue;
+        }
         if (fused) {
             // FE (which also forms u_2), then n/2 launches of two substeps:
             // (LF1, LF2), ..., (LF_{n-1}, final).  Field slots: y1 -> buffer 2; the

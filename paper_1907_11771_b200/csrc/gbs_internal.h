@@ -57,7 +57,9 @@ struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
     double* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // Y, ACC, L0..L3 (+ ghosts)
     bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
-    CUtensorMap tm[6][3][3];          // [buffer][field][box shape A/B/C] (TMA kernels)
+    // [buffer][field][box]: 64x16, 64xr, rx16 (all TMA kernels); 2-D two-substep kernels also
+    // 64x(16+2r), rx(16+2r), 64x(16+4r), rx(16+4r)
+    CUtensorMap tm[6][3][7];
 };
 
 constexpr int kClusterMaxN = 7000;     // 4 nx doubles of shared memory per CTA
@@ -120,10 +122,14 @@ struct gbs_ctx {
     int* d_nk = nullptr;              // step counts / half weights for the cluster kernel
     double* d_wh = nullptr;
     bool use_fuse = true;             // two-substep (temporally blocked) kernels where eligible
+    bool use_fuse2d = false;          // 2-D chain pair kernels (measured slower: opt-in)
                                       // (bit-exact)
     bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
     int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
+    int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
+    int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
+    int band_opt = 0;                 // 3-D TMA tile launch order (0 = whole rows)
     int sms = 148;                    // streaming multiprocessors of the device
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     double graph_H = -1.0;
@@ -199,6 +205,11 @@ int64_t state_bytes(const gbs_ctx* c);  // device bytes of the state buffers of 
 void free_state(gbs_ctx* c);
 int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi);
 int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi);
+// ghost rows of a single slab from its own opposite side, for (buffer, field mask) pairs
+int launch_ghost_fill(gbs_ctx* c, const std::vector<std::pair<int, unsigned>>& halos);
+// 2-D acoustics, two leap-frog substeps (P, S buffers -> A = y_{n+1}, B = y_{n+2} buffers)
+int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, double cfA, double cfB, int64_t lo,
+                     int64_t hi);
 bool persistent_path(const gbs_ctx* c);
 int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);
 // ---- gbs_exec.cu

@@ -112,6 +112,9 @@ struct Wave3DArgs {
     int* nonfinite;          // optional flag (FIN modes)
     double* Xu;              // optional (FE, TMA kernel): u_2 = S_u + cf2 * v_1, the first
     double cf2;              // leap-frog step's u-component, for the two-substep kernel
+    int band;                // TMA kernels: launch order of the x-y tiles (tma::tile_of)
+    int hint;                // TMA kernel L2 policy bits: 1 u tiles evict_last, 2 pointwise
+                             // boxes evict_first, 8 streaming (.cs) stores
 };
 
 template <int R, int MODE, int VX, int BY, bool SLAB>
@@ -361,6 +364,27 @@ acoustic2d_step(const Acoustic2DArgs A) {
     }
     if constexpr (MODE == MODE_FIN0 || MODE == MODE_FINACC)
         if (bad && valid && A.nonfinite) *A.nonfinite = 1;
+}
+
+// ===========================================================================
+// Ghost rows/planes of a single slab from its own periodic opposite side (the
+// 2-D two-substep kernels read 2r rows beyond their bands): for each listed
+// field, ghosts [-g, 0) <- [n - g, n) and [n, n + g) <- [0, g), plane = points per row/plane.
+// ===========================================================================
+struct GhostFillArgs {
+    double* f[6];            // field bases (interior row 0)
+    int nf;
+    int64_t n, g, plane;
+};
+
+static __global__ void __launch_bounds__(256) ghost_fill(const GhostFillArgs A) {
+    const int64_t per = A.g * A.plane;                       // values per side per field
+    const int which = blockIdx.y;                            // field
+    double* base = A.f[which];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
+        base[i - per] = base[(A.n - A.g) * A.plane + i];     // below row 0 <- top rows
+        base[A.n * A.plane + i] = base[i];                   // above row n-1 <- bottom rows
+    }
 }
 
 // ===========================================================================

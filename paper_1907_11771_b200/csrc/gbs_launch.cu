@@ -7,6 +7,7 @@
 #include "gbs_wave3d_tma.cuh"
 #include "gbs_wave3d_pair.cuh"
 #include "gbs_acoustic2d_tma.cuh"
+#include "gbs_acoustic2d_pair.cuh"
 #include "gbs_adv1d_cluster.cuh"
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -47,14 +48,18 @@ int alloc_state(gbs_ctx* c) {
     int nloc = c->loopback;
     int64_t total_slabs = (int64_t)c->slabs * nloc;
     int64_t nzl = c->nslow / total_slabs;
-    c->ghost = total_slabs > 1 ? c->R : 0;
+    // 2-D TMA grids keep 2r ghost rows even on one slab (a self-exchange refreshes them): the
+    // two-substep 2-D kernels read 2r rows beyond their bands and never wrap in y
+    const bool ac2d_tma = c->pde == GBS_ACOUSTIC2D && c->n[0] % gbs::tma::TX == 0 && nzl % gbs::tma::TY == 0 &&
+                          nzl >= 4 * c->R;
+    c->ghost = ac2d_tma ? 2 * c->R : (total_slabs > 1 ? c->R : 0);
     c->field_stride = (nzl + 2 * c->ghost) * c->plane;
     // the TMA (and two-substep) kernels need the grid to be a multiple of their tile so
     // halo boxes never cross the wrap; the two-substep kernels need 4 level buffers
     // (2-D acoustics: x a multiple of the tile width, each slab's rows a multiple of its height)
     c->tma_grid = (c->pde == GBS_WAVE3D && c->n[0] % gbs::tma::TX == 0 && c->n[1] % gbs::tma::TY == 0) ||
                   (c->pde == GBS_ACOUSTIC2D && c->n[0] % gbs::tma::TX == 0 && nzl % gbs::tma::TY == 0);
-    c->nbuf = (c->tma_grid && c->pde == GBS_WAVE3D) ? 6 : 4;
+    c->nbuf = c->tma_grid ? 6 : 4;
     c->slab.assign(nloc, Slab());
     for (int v = 0; v < nloc; ++v) {
         Slab& s = c->slab[v];
@@ -110,6 +115,11 @@ int ensure_buffers(gbs_ctx* c) {
                     ok = make_map(&s.tm[b][f][0], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY) &&
                          make_map(&s.tm[b][f][1], base, c->n[0], vy, vz, gbs::tma::TX, c->R) &&
                          make_map(&s.tm[b][f][2], base, c->n[0], vy, vz, c->R, gbs::tma::TY);
+                    if (ok && c->pde == GBS_ACOUSTIC2D)
+                        ok = make_map(&s.tm[b][f][3], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY + 2 * c->R) &&
+                             make_map(&s.tm[b][f][4], base, c->n[0], vy, vz, c->R, gbs::tma::TY + 2 * c->R) &&
+                             make_map(&s.tm[b][f][5], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY + 4 * c->R) &&
+                             make_map(&s.tm[b][f][6], base, c->n[0], vy, vz, c->R, gbs::tma::TY + 4 * c->R);
                 }
             s.tma_ok = ok;
         }
@@ -193,6 +203,13 @@ static void launch_ac2d(const gbs::Acoustic2DArgs& a, dim3 grid, bool vx2, cudaS
     else gbs::acoustic2d_step<R, MODE, 1, 128, SLAB><<<grid, 128, 0, st>>>(a);
 }
 
+// x-tiles per launch-order band of the 3-D TMA kernels (tma::tile_of): option "band"
+// when it divides the tile count, else whole rows
+static int tile_band(const gbs_ctx* c, int64_t ntx) {
+    const int b = c->band_opt;
+    return (b > 0 && ntx % b == 0) ? b : (int)ntx;
+}
+
 static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
     if (zchunk_opt > 0) return (int)std::min<int64_t>(zchunk_opt, extent);
     // aim at >= ~16 resident waves of CTAs so the tail stays small, with
@@ -205,10 +222,12 @@ static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
 
 // one substep over the planes [lo, hi) of slab s (lo = 0, hi = s.nz: the whole slab)
 int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi) {
-    const bool slab = c->ghost > 0;
+    // slab kernels read ghost planes refreshed from neighbours; one slab (2-D TMA grids keep
+    // ghost rows for the two-substep kernels) wraps periodically like a plain grid
+    const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
     int* flag = op.flag ? c->d_flag : nullptr;
     if (c->pde == GBS_WAVE3D) {
-        gbs::Wave3DArgs a;
+        gbs::Wave3DArgs a{};
         a.Su = field_ptr(c, s, op.S, 0); a.Sv = field_ptr(c, s, op.S, 1);
         a.Pu = field_ptr(c, s, op.P, 0); a.Pv = field_ptr(c, s, op.P, 1);
         a.Ou = field_ptr(c, s, op.O, 0); a.Ov = field_ptr(c, s, op.O, 1);
@@ -225,7 +244,9 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
             a.zlo = (int)lo; a.zhi = (int)hi;
             a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo)
                                          : (int)std::min<int64_t>(128, hi - lo);
-            dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+            a.band = tile_band(c, tx);
+            a.hint = c->hint_step_opt;
+            dim3 grid((unsigned)(tx * ty), 1u, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
             gbs::tma::Maps m;
             m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
             m.sv = s.tm[op.S][1][0];
@@ -343,7 +364,9 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
 }
 
 int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi) {
-    const bool slab = c->ghost > 0;
+    // slab kernels read ghost planes refreshed from neighbours; one slab (2-D TMA grids keep
+    // ghost rows for the two-substep kernels) wraps periodically like a plain grid
+    const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
     const bool lf = op.modeB == gbs::MODE_LF;
     gbs::tma::PairArgs a;
     if (lf) {
@@ -364,7 +387,9 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     a.nonfinite = op.flag ? c->d_flag : nullptr;
     a.zlo = (int)lo; a.zhi = (int)hi;
     a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo) : (int)std::min<int64_t>(128, hi - lo);
-    dim3 grid((unsigned)(c->n[0] / gbs::tma::TX), (unsigned)(c->n[1] / gbs::tma::TY),
+    a.band = tile_band(c, c->n[0] / gbs::tma::TX);
+    a.hint = c->hint_opt;
+    dim3 grid((unsigned)((c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY)), 1u,
               (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
     gbs::tma::PairMaps m;
     m.su_a = s.tm[op.Su.b][op.Su.f][0]; m.su_b = s.tm[op.Su.b][op.Su.f][1]; m.su_c = s.tm[op.Su.b][op.Su.f][2];
@@ -385,6 +410,82 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
 #undef PR
     if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "pair kernel setup: %s", cudaGetErrorString(e));
     c->launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
+int launch_ghost_fill(gbs_ctx* c, const std::vector<std::pair<int, unsigned>>& halos) {
+    gbs::GhostFillArgs a{};
+    Slab& s = c->slab[0];
+    for (auto& h : halos)
+        for (int f = 0; f < c->F; ++f)
+            if ((h.second >> f) & 1u) {
+                if (a.nf == 6) return fail(c, GBS_E_INVAL, "ghost_fill: more than 6 fields");
+                a.f[a.nf++] = field_ptr(c, s, h.first, f);
+            }
+    if (!a.nf) return GBS_OK;
+    a.n = s.nz; a.g = c->ghost; a.plane = c->plane;
+    const int64_t per = a.g * a.plane;
+    dim3 grid((unsigned)std::min<int64_t>((per + 255) / 256, 4 * c->sms), (unsigned)a.nf);
+    gbs::ghost_fill<<<grid, 256, 0, c->stream>>>(a);
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "ghost fill launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// 2-D acoustics, two leap-frog substeps per pass (gbs_acoustic2d_pair.cuh): the
+// chain-U kernel then the chain-P kernel over the rows [lo, hi) of slab s
+// ---------------------------------------------------------------------------
+template <int R>
+static cudaError_t launch_ac2d_chains(const gbs::tma::Ac2PairMaps& m, const gbs::tma::Ac2PairArgs& a, int ybase,
+                                      dim3 grid, cudaStream_t st) {
+    using LU = gbs::tma::ChainULayout<R>;
+    using LP = gbs::tma::ChainPLayout<R>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gbs::tma::acoustic2d_chainU_tma<R>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LU::bytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(gbs::tma::acoustic2d_chainP_tma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)LP::bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const dim3 block(32, gbs::tma::AC2_NW + 1);
+    gbs::tma::acoustic2d_chainU_tma<R><<<grid, block, LU::bytes, st>>>(m, a, ybase);
+    gbs::tma::acoustic2d_chainP_tma<R><<<grid, block, LP::bytes, st>>>(m, a, ybase);
+    return cudaSuccess;
+}
+
+int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, double cfA, double cfB, int64_t lo,
+                     int64_t hi) {
+    gbs::tma::Ac2PairArgs a;
+    for (int f = 0; f < 3; ++f) {
+        a.A[f] = field_ptr(c, s, Aout, f);
+        a.B[f] = field_ptr(c, s, Bout, f);
+    }
+    a.nx = (int)c->n[0]; a.ny = (int)s.nz;
+    a.ylo = (int)lo; a.yhi = (int)hi;
+    a.sx = c->n[0] / c->len[0]; a.sy = c->n[1] / c->len[1];
+    a.cfA = cfA; a.cfB = cfB;
+    const int64_t xt = c->n[0] / gbs::tma::TX;
+    a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms);
+    dim3 grid((unsigned)xt, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
+    gbs::tma::Ac2PairMaps m;
+    static const int pick[6] = {0, 2, 3, 4, 5, 6};      // Ac2PairMaps box order -> tm shape index
+    for (int f = 0; f < 3; ++f)
+        for (int k = 0; k < 6; ++k) {
+            m.s[f][k] = s.tm[S][f][pick[k]];
+            m.p[f][k] = s.tm[P][f][pick[k]];
+        }
+    const int ybase = (int)c->ghost;
+    cudaError_t e = c->R == 2 ? launch_ac2d_chains<2>(m, a, ybase, grid, c->stream)
+                              : launch_ac2d_chains<4>(m, a, ybase, grid, c->stream);
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "2-D pair kernel setup: %s", cudaGetErrorString(e));
+    c->launches += 2;
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return GBS_OK;

@@ -78,6 +78,9 @@ struct PairArgs {
     double sx2, sy2, sz2;
     double cfA, cfB, wh;
     int* nonfinite;
+    int band;                         // launch order of the x-y tiles (tile_of)
+    int hint;                         // L2 policy bits (experiment): 1 fronts evict_last,
+                                      // 2 pointwise evict_first, 4 tiles evict_first, 8 .cs stores
 };
 
 template <int R, int MODEB, bool SLAB>
@@ -94,7 +97,9 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
 
     const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
     const int nx = A.nx, ny = A.ny, nz = A.nz;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    int xt, yt;
+    tile_of(blockIdx.x, nx / TX, ny / TY, A.band, xt, yt);
+    const int x0 = xt * TX, y0 = yt * TY;
     const int z0 = A.zlo + blockIdx.z * A.zchunk;
     const int niter = min(A.zchunk, A.zhi - z0);
     auto zc = [&](int z) -> int {
@@ -112,13 +117,18 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
     const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
 
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    auto ld = [&](void* dst, const CUtensorMap* m, int x, int y, int z, uint64_t* bar, int bit, uint64_t pol) {
+        if (A.hint & bit) tma_load_3d_hint(dst, m, x, y, z, bar, pol);
+        else tma_load_3d(dst, m, x, y, z, bar);
+    };
     auto load_tile = [&](double* dst, const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int z,
                          uint64_t* bar) {
-        tma_load_3d(dst, b, x0, ytop, z, bar);
-        tma_load_3d(dst + R * TX, a, x0, y0, z, bar);
-        tma_load_3d(dst + (R + TY) * TX, b, x0, ybot, z, bar);
-        tma_load_3d(dst + L::CENTER, c, xl, y0, z, bar);
-        tma_load_3d(dst + L::CENTER + L::STRIP, c, xr, y0, z, bar);
+        ld(dst, b, x0, ytop, z, bar, 4, pol_first);
+        ld(dst + R * TX, a, x0, y0, z, bar, 4, pol_first);
+        ld(dst + (R + TY) * TX, b, x0, ybot, z, bar, 4, pol_first);
+        ld(dst + L::CENTER, c, xl, y0, z, bar, 4, pol_first);
+        ld(dst + L::CENTER + L::STRIP, c, xr, y0, z, bar, 4, pol_first);
     };
     auto issue_stage = [&](int i) {
         const int s = i % D;
@@ -128,13 +138,13 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         const int z = zc(z0 + i), zf = zc(z0 + i + R);
         load_tile(st, &M.su_a, &M.su_b, &M.su_c, z, &full[s]);
         load_tile(st + L::O_UT, &M.u_a, &M.u_b, &M.u_c, z, &full[s]);
-        tma_load_3d(st + L::O_SUF, &M.su_a, x0, y0, zf, &full[s]);
-        tma_load_3d(st + L::O_UF, &M.u_a, x0, y0, zf, &full[s]);
-        tma_load_3d(st + L::O_SV, &M.sv, x0, y0, z, &full[s]);
-        tma_load_3d(st + L::O_PV, &M.pv, x0, y0, z, &full[s]);
+        ld(st + L::O_SUF, &M.su_a, x0, y0, zf, &full[s], 1, pol_last);
+        ld(st + L::O_UF, &M.u_a, x0, y0, zf, &full[s], 1, pol_last);
+        ld(st + L::O_SV, &M.sv, x0, y0, z, &full[s], 2, pol_first);
+        ld(st + L::O_PV, &M.pv, x0, y0, z, &full[s], 2, pol_first);
         if constexpr (MODEB == MODE_FINACC) {
-            tma_load_3d(st + L::O_AC, &M.acc_u, x0, y0, z, &full[s]);
-            tma_load_3d(st + L::O_AC + L::PWT, &M.acc_v, x0, y0, z, &full[s]);
+            ld(st + L::O_AC, &M.acc_u, x0, y0, z, &full[s], 2, pol_first);
+            ld(st + L::O_AC + L::PWT, &M.acc_v, x0, y0, z, &full[s], 2, pol_first);
         }
     };
 
@@ -266,6 +276,15 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int64_t o = oz + own + (int64_t)r * nx;
+            if (A.hint & 8) {
+                if constexpr (MODEB == MODE_LF) {
+                    __stcs(reinterpret_cast<double2*>(A.Av + o), make_double2(va[2 * r], va[2 * r + 1]));
+                    __stcs(reinterpret_cast<double2*>(A.Cu + o), make_double2(uc[2 * r], uc[2 * r + 1]));
+                }
+                __stcs(reinterpret_cast<double2*>(A.Bu + o), make_double2(ub[2 * r], ub[2 * r + 1]));
+                __stcs(reinterpret_cast<double2*>(A.Bv + o), make_double2(vb[2 * r], vb[2 * r + 1]));
+                continue;
+            }
             if constexpr (MODEB == MODE_LF) {
                 *reinterpret_cast<double2*>(A.Av + o) = make_double2(va[2 * r], va[2 * r + 1]);
                 *reinterpret_cast<double2*>(A.Cu + o) = make_double2(uc[2 * r], uc[2 * r + 1]);

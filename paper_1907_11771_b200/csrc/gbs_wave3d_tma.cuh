@@ -62,6 +62,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                                 uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -70,6 +89,18 @@ template <int MODE> struct NPW { static constexpr int v = (MODE == MODE_FE) ? 1 
 template <int MODE> struct Depth { static constexpr int v = (MODE == MODE_FINACC) ? 3 : 4; };
 
 constexpr int TX = 64, TY = 16;
+
+// Launch order of the ntx x nty tiles of a plane (grid x = ntx * nty): bands of `band`
+// x-tiles, x fastest inside a band, then y, then the next band.  band = ntx is plain
+// row order.  Resident CTAs start in launch order and march z at the same rate, so two
+// tiles k launches apart run ~k/148 of a CTA lifetime apart in z: the band keeps the
+// y-neighbours (whose halo rows a tile reads from L2) band launches apart instead of ntx.
+__device__ __forceinline__ void tile_of(int L, int ntx, int nty, int band, int& xt, int& yt) {
+    const int per = band * nty;
+    const int b = L / per, r = L - b * per;
+    yt = r / band;
+    xt = b * band + (r - yt * band);
+}
 
 template <int R, int MODE>
 struct Layout {
@@ -110,9 +141,9 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
 
     const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
     const int nx = A.nx, ny = A.ny, nz = A.nz;
-    // x-tiles vary fastest in the launch order: resident CTAs stream whole rows
-    // (DRAM page locality; y-fastest order measured 10% slower on 1024^3)
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    int xt, yt;
+    tile_of(blockIdx.x, nx / TX, ny / TY, A.band, xt, yt);
+    const int x0 = xt * TX, y0 = yt * TY;
     const int z0 = A.zlo + blockIdx.z * A.zchunk;
     const int niter = min(A.zchunk, A.zhi - z0);
 
@@ -136,14 +167,19 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
         if constexpr (MODE == MODE_FINACC) { prefetch_map(&M.au); prefetch_map(&M.av); }
         const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
         const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
+        const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+        auto ld = [&](void* dst, const CUtensorMap* m, int x, int y, int z, uint64_t* bar, int bit, uint64_t pol) {
+            if (A.hint & bit) tma_load_3d_hint(dst, m, x, y, z, bar, pol);
+            else tma_load_3d(dst, m, x, y, z, bar);
+        };
         auto issue_tile = [&](int p, uint64_t* bar) {
             double* t = ring + (size_t)(p % RING) * TILE;
             const int z = zc(z0 + p);
-            tma_load_3d(t, &M.su_b, x0, ytop, z, bar);
-            tma_load_3d(t + R * TX, &M.su_a, x0, y0, z, bar);
-            tma_load_3d(t + (R + TY) * TX, &M.su_b, x0, ybot, z, bar);
-            tma_load_3d(t + L::CENTER, &M.su_c, xl, y0, z, bar);
-            tma_load_3d(t + L::CENTER + L::STRIP, &M.su_c, xr, y0, z, bar);
+            ld(t, &M.su_b, x0, ytop, z, bar, 1, pol_last);
+            ld(t + R * TX, &M.su_a, x0, y0, z, bar, 1, pol_last);
+            ld(t + (R + TY) * TX, &M.su_b, x0, ybot, z, bar, 1, pol_last);
+            ld(t + L::CENTER, &M.su_c, xl, y0, z, bar, 1, pol_last);
+            ld(t + L::CENTER + L::STRIP, &M.su_c, xr, y0, z, bar, 1, pol_last);
         };
         mbar_expect_tx(init, R * L::tile_bytes);
         for (int p = 0; p < R; ++p) issue_tile(p, init);
@@ -154,14 +190,14 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
             issue_tile(i + R, &full[s]);
             double* p = pw + (size_t)s * NP * PWT;
             const int z = zc(z0 + i);
-            tma_load_3d(p, &M.sv, x0, y0, z, &full[s]);
+            ld(p, &M.sv, x0, y0, z, &full[s], 2, pol_first);
             if constexpr (MODE != MODE_FE) {
-                tma_load_3d(p + PWT, &M.pu, x0, y0, z, &full[s]);
-                tma_load_3d(p + 2 * PWT, &M.pv, x0, y0, z, &full[s]);
+                ld(p + PWT, &M.pu, x0, y0, z, &full[s], 2, pol_first);
+                ld(p + 2 * PWT, &M.pv, x0, y0, z, &full[s], 2, pol_first);
             }
             if constexpr (MODE == MODE_FINACC) {
-                tma_load_3d(p + 3 * PWT, &M.au, x0, y0, z, &full[s]);
-                tma_load_3d(p + 4 * PWT, &M.av, x0, y0, z, &full[s]);
+                ld(p + 3 * PWT, &M.au, x0, y0, z, &full[s], 2, pol_first);
+                ld(p + 4 * PWT, &M.av, x0, y0, z, &full[s], 2, pol_first);
             }
         }
         return;
@@ -250,15 +286,19 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
                 bad |= !isfinite(ou[v]) || !isfinite(ov[v]);
         }
         const int64_t o = zoff(z0 + i) + own;
-        *reinterpret_cast<double2*>(A.Ou + o) = make_double2(ou[0], ou[1]);
-        *reinterpret_cast<double2*>(A.Ov + o) = make_double2(ov[0], ov[1]);
+        const bool cs = A.hint & 8;
+        auto put = [&](double* p, double a, double b) {
+            if (cs) __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
+            else *reinterpret_cast<double2*>(p) = make_double2(a, b);
+        };
+        put(A.Ou + o, ou[0], ou[1]);
+        put(A.Ov + o, ov[0], ov[1]);
         if constexpr (MODE == MODE_FE) {
             // u_2 = u_0 + 2h v_1 (the next leap-frog step's pointwise u, formed exactly as
             // the single-step LF kernel forms it) for the two-substep kernel
             if (A.Xu)
-                *reinterpret_cast<double2*>(A.Xu + o) =
-                    make_double2(combine<MODE_LF>(xw[R], 0.0, ov[0], 0.0, A.cf2, 0.0),
-                                 combine<MODE_LF>(xw[R + 1], 0.0, ov[1], 0.0, A.cf2, 0.0));
+                put(A.Xu + o, combine<MODE_LF>(xw[R], 0.0, ov[0], 0.0, A.cf2, 0.0),
+                    combine<MODE_LF>(xw[R + 1], 0.0, ov[1], 0.0, A.cf2, 0.0));
         }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j) q[j] = q[j + 1];

@@ -149,6 +149,25 @@ def test_2d_bulk_kernel_bitwise_equals_register_kernel(torch_cuda, cfg, n):
     assert np.array_equal(a[0], b[0])
 
 
+@pytest.mark.parametrize("cfg,n,opts", [("c3", (128, 64, 1), {}), ("c2", (128, 96, 1), {}),
+                                        ("c3", (64, 48, 1), {}), ("c3", (192, 96, 1), {"loopback": 2}),
+                                        ("c2", (128, 96, 1), {"loopback": 3, "overlap": 0}),
+                                        ("c3", (64, 32, 1), {"graph": 0})])
+def test_2d_two_substep_kernels_bitwise_equal_single_steps(torch_cuda, cfg, n, opts):
+    """2-D acoustics, two leap-frog substeps per pass (the chain-U and chain-P kernels,
+    gbs_acoustic2d_pair.cuh): bit-identical to single-step launches, and the oracle's result."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fuse2d=1))
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fuse2d=0))
+    assert np.array_equal(a[0], b[0])
+    # FE + LF1 + FIN single and (n-2)/2 pairs of two chain kernels: as many stencil launches
+    # as substeps, plus (single-slab grids) one ghost-row fill per pair
+    assert ia["kernel_launches"] >= ib["kernel_launches"]
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(a[0], o[0], what=f"2-D pairs {cfg} {n} {opts}")
+
+
 @pytest.mark.parametrize("cfg,n", [("c4", (128, 32, 24)), ("c4", (64, 16, 17)), ("c5", (64, 48, 40))])
 def test_two_substep_kernel_bitwise_equals_single_steps(torch_cuda, cfg, n):
     """The temporally blocked kernel (two substeps per HBM pass) recomputes the
