@@ -19,10 +19,13 @@
 // Layout: slab mode only (ghost rows of r on each side of the y axis, refreshed
 // before every launch; one slab = a self-exchange), so every box lies inside the
 // tensor; x halos are separate column blocks at wrapped coordinates.  A CTA
-// covers 64 columns and marches y in 16-row bands; 8 consumer warps work on 2 x 2
-// point blocks (rows r, r+1 and columns c, c+1: 128-bit shared loads, y windows
-// shared by the two rows), 1 producer warp issues one TMA box per column block
-// per field, D = 3 stages.
+// covers 64 columns and marches y in AC2_BH = 32-row bands (the intermediate level's
+// halo overhead is (32 + 2r) / 32 instead of (16 + 2r) / 16); 16 consumer warps work on
+// 2 x 2 point blocks (rows r, r+1 and columns c, c+1: 128-bit shared loads, y windows
+// shared by the two rows) in two phases per band -- the intermediate level on the
+// extended band, then the band's output (one block per thread) -- with the items of a
+// phase spread over all consumer threads; 1 producer warp issues one TMA box per column
+// block per field, D = 2 stages (shared memory).
 #pragma once
 
 #include "gbs_wave3d_tma.cuh"
@@ -32,15 +35,19 @@ namespace tma {
 
 __host__ __device__ constexpr int pad16(int x) { return (x + 15) / 16 * 16; }   // 128-byte blocks
 
+constexpr int AC2_BH = 32;                        // rows per band
+constexpr int AC2_NW = 16;                        // consumer warps (+ 1 producer warp)
+
 template <int R>
 struct Ac2Geom {
-    static constexpr int NRU = TY + 2 * R;        // rows [-r, 16 + r)
-    static constexpr int NRV = TY + 4 * R;        // rows [-2r, 16 + 2r)
+    static constexpr int BH = AC2_BH;
+    static constexpr int NRU = BH + 2 * R;        // rows [-r, BH + r)
+    static constexpr int NRV = BH + 4 * R;        // rows [-2r, BH + 2r)
     static constexpr int WA = TX + 2 * R;         // cols [-r, 64 + r)
 };
 
-// chain U stage: S_u (rows [-r,16+r); blocks at cols -2r, -r, 0, 64, 64+r), S_v (rows
-// [-2r,16+2r); cols -r, 0, 64), P_p (rows [-r,16+r); cols -r, 0, 64)
+// chain U stage: S_u (rows [-r,BH+r); blocks at cols -2r, -r, 0, 64, 64+r), S_v (rows
+// [-2r,BH+2r); cols -r, 0, 64), P_p (rows [-r,BH+r); cols -r, 0, 64)
 template <int R>
 struct ChainULayout {
     using G = Ac2Geom<R>;
@@ -50,32 +57,33 @@ struct ChainULayout {
     static constexpr int SV = SU + 4 * BU + CU;                        // L1 | C | R1
     static constexpr int PP = SV + 2 * BV + CV;                        // L1 | C | R1
     static constexpr int STAGE = PP + 2 * BU + CU;
-    static constexpr int D = 3;
+    static constexpr int D = 2;
     static constexpr int SCR = G::NRU * G::WA;                         // A_p scratch
     static constexpr size_t bytes = ((size_t)D * STAGE + SCR) * 8 + 2 * D * 8;
     static constexpr uint32_t stage_bytes =
         (uint32_t)(4 * G::NRU * R + G::NRU * TX + 2 * G::NRV * R + G::NRV * TX + 2 * G::NRU * R + G::NRU * TX) * 8;
 };
 
-// chain P stage: S_p (centre rows [-2r,16+2r); strips at cols -2r, -r, 64, 64+r on the band
-// rows), P_u (band rows; cols -r, 0, 64), P_v (rows [-r,16+r); band columns)
+// chain P stage: S_p (centre rows [-2r,BH+2r); strips at cols -2r, -r, 64, 64+r on the band
+// rows), P_u (band rows; cols -r, 0, 64), P_v (rows [-r,BH+r); band columns)
 template <int R>
 struct ChainPLayout {
     using G = Ac2Geom<R>;
-    static constexpr int BS = pad16(TY * R);
+    static constexpr int BS = pad16(G::BH * R);
     static constexpr int SPC = 0, SPS = G::NRV * TX;                   // centre | L2 L1 R1 R2
     static constexpr int PU = SPS + 4 * BS;                            // L1 | C | R1
-    static constexpr int PV = PU + 2 * BS + TY * TX;
+    static constexpr int PV = PU + 2 * BS + G::BH * TX;
     static constexpr int STAGE = PV + G::NRU * TX;
-    static constexpr int D = 3;
-    static constexpr int SCR_U = TY * G::WA, SCR_V = G::NRU * TX;      // A_u, A_v scratch
+    static constexpr int D = 2;
+    static constexpr int SCR_U = G::BH * G::WA, SCR_V = G::NRU * TX;   // A_u, A_v scratch
     static constexpr size_t bytes = ((size_t)D * STAGE + SCR_U + SCR_V) * 8 + 2 * D * 8;
-    static constexpr uint32_t stage_bytes = (uint32_t)(G::NRV * TX + 4 * TY * R + 2 * TY * R + TY * TX + G::NRU * TX) * 8;
+    static constexpr uint32_t stage_bytes =
+        (uint32_t)(G::NRV * TX + 4 * G::BH * R + 2 * G::BH * R + G::BH * TX + G::NRU * TX) * 8;
 };
 
 struct Ac2PairMaps {
     // per field (p, u, v) of the current level S and the previous level P:
-    //   [0] 64 x 16, [1] r x 16, [2] 64 x (16+2r), [3] r x (16+2r), [4] 64 x (16+4r), [5] r x (16+4r)
+    //   [0] 64 x BH, [1] r x BH, [2] 64 x (BH+2r), [3] r x (BH+2r), [4] 64 x (BH+4r), [5] r x (BH+4r)
     CUtensorMap s[3][6];
     CUtensorMap p[3][6];
 };
@@ -84,7 +92,7 @@ struct Ac2PairArgs {
     double* A[3];            // y_{n+1} (p, u, v)
     double* B[3];            // y_{n+2}
     int nx, ny;              // ny = local slab rows
-    int ylo, yhi, ychunk;    // rows [ylo, yhi) of the slab, ychunk rows per CTA (multiples of 16)
+    int ylo, yhi, ychunk;    // rows [ylo, yhi) of the slab, ychunk rows per CTA (multiples of BH)
     double sx, sy, cfA, cfB;
 };
 
@@ -102,12 +110,9 @@ struct Cols {
     }
 };
 
-constexpr int AC2_NW = 16;                        // consumer warps (+ 1 producer warp)
-
 // barrier of the consumer warps only (the producer warp has returned)
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * AC2_NW) : "memory"); }
 
-template <int R>
 __device__ __forceinline__ void ldpair(const double* p, double& a, double& b) {
     const double2 t = *reinterpret_cast<const double2*>(p);
     a = t.x; b = t.y;
@@ -119,7 +124,7 @@ __global__ void __launch_bounds__(32 * (AC2_NW + 1), 1)
 acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A, const int ybase) {
     using L = ChainULayout<R>;
     using G = Ac2Geom<R>;
-    constexpr int D = L::D, NW = AC2_NW;
+    constexpr int D = L::D, NW = AC2_NW, BH = G::BH;
     extern __shared__ __align__(128) double smem[];
     double* scr = smem + (size_t)D * L::STAGE;
     uint64_t* full = reinterpret_cast<uint64_t*>(scr + L::SCR);
@@ -128,7 +133,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
     const int nx = A.nx;
     const int x0 = blockIdx.x * TX;
     const int ys = A.ylo + blockIdx.y * A.ychunk;
-    const int niter = min(A.ychunk, A.yhi - ys) / TY;
+    const int niter = min(A.ychunk, A.yhi - ys) / BH;
     const Cols<R, 5> su{{-2 * R, -R, 0, TX, TX + R}, {R, R, TX, R, R},
                         {L::SU, L::SU + L::BU, L::SU + 2 * L::BU, L::SU + 2 * L::BU + L::CU, L::SU + 3 * L::BU + L::CU}};
     const Cols<R, 3> sv{{-R, 0, TX}, {R, TX, R}, {L::SV, L::SV + L::BV, L::SV + L::BV + L::CV}};
@@ -149,7 +154,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             if (i >= D) mbar_wait(&empty[s], (uint32_t)(((i / D) - 1) & 1));
             mbar_expect_tx(&full[s], L::stage_bytes);
             double* st = smem + (size_t)s * L::STAGE;
-            const int y = ys + i * TY + ybase;             // tensor row of the band's first row
+            const int y = ys + i * BH + ybase;             // tensor row of the band's first row
             const int yu = y - R, yv = y - 2 * R;
             tma_load_3d(st + su.base[0], &M.s[1][3], xl2, yu, 0, &full[s]);
             tma_load_3d(st + su.base[1], &M.s[1][3], xl1, yu, 0, &full[s]);
@@ -165,13 +170,13 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
         }
         return;
     }
-    // ============================ consumers (8 warps) ============================
+    // ============================ consumers ============================
     constexpr int NT = 32 * NW;
     for (int i = 0; i < niter; ++i) {
         const int s = i % D;
         mbar_wait(&full[s], (uint32_t)((i / D) & 1));
         const double* st = smem + (size_t)s * L::STAGE;
-        // phase 1: A_p on rows [-r, 16+r) x cols [-r, 64+r), 2 x 2 points per item
+        // phase 1: A_p on rows [-r, BH+r) x cols [-r, 64+r), 2 x 2 points per item
         constexpr int QR = G::NRU / 2, QC = G::WA / 2;
         for (int it = tid; it < QR * QC; it += NT) {
             const int r = -R + 2 * (it / QC), c = -R + 2 * (it % QC);
@@ -180,7 +185,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             for (int h = 0; h < 2; ++h) {
                 double w[2 * R + 2];
 #pragma unroll
-                for (int k = 0; k <= R; ++k) ldpair<R>(su.at(st, r + h + R, c - R + 2 * k), w[2 * k], w[2 * k + 1]);
+                for (int k = 0; k <= R; ++k) ldpair(su.at(st, r + h + R, c - R + 2 * k), w[2 * k], w[2 * k + 1]);
 #pragma unroll
                 for (int j = 1; j <= R; ++j)
 #pragma unroll
@@ -188,7 +193,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             }
             double col[2 * R + 2][2];                     // S_v rows r-R .. r+1+R at cols c, c+1
 #pragma unroll
-            for (int k = 0; k < 2 * R + 2; ++k) ldpair<R>(sv.at(st, r - R + k + 2 * R, c), col[k][0], col[k][1]);
+            for (int k = 0; k < 2 * R + 2; ++k) ldpair(sv.at(st, r - R + k + 2 * R, c), col[k][0], col[k][1]);
 #pragma unroll
             for (int j = 1; j <= R; ++j)
 #pragma unroll
@@ -199,7 +204,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 double p0, p1;
-                ldpair<R>(pp.at(st, r + h + R, c), p0, p1);
+                ldpair(pp.at(st, r + h + R, c), p0, p1);
                 const double pv[2] = {p0, p1};
                 double ap[2];
 #pragma unroll
@@ -209,16 +214,16 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             }
         }
         consumers_sync();
-        // phase 2: B_u, B_v on the band (16 x 64), one 2 x 2 item per thread
-        if (tid < (TY / 2) * (TX / 2)) {
-            const int r = 2 * (tid / (TX / 2)), c = 2 * (tid % (TX / 2));
+        // phase 2: B_u, B_v on the band (BH x 64), 2 x 2 items
+        for (int it = tid; it < (BH / 2) * (TX / 2); it += NT) {
+            const int r = 2 * (it / (TX / 2)), c = 2 * (it % (TX / 2));
             double dxp[2][2] = {{0, 0}, {0, 0}}, dyp[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 double w[2 * R + 2];
 #pragma unroll
                 for (int k = 0; k <= R; ++k)
-                    ldpair<R>(scr + (r + h + R) * G::WA + (c - R + 2 * k + R), w[2 * k], w[2 * k + 1]);
+                    ldpair(scr + (r + h + R) * G::WA + (c - R + 2 * k + R), w[2 * k], w[2 * k + 1]);
 #pragma unroll
                 for (int j = 1; j <= R; ++j)
 #pragma unroll
@@ -227,7 +232,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             double col[2 * R + 2][2];                     // A_p rows r-R .. r+1+R at cols c, c+1
 #pragma unroll
             for (int k = 0; k < 2 * R + 2; ++k)
-                ldpair<R>(scr + (r - R + k + R) * G::WA + (c + R), col[k][0], col[k][1]);
+                ldpair(scr + (r - R + k + R) * G::WA + (c + R), col[k][0], col[k][1]);
 #pragma unroll
             for (int j = 1; j <= R; ++j)
 #pragma unroll
@@ -235,12 +240,12 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
 #pragma unroll
                     for (int e = 0; e < 2; ++e)
                         dyp[h][e] = fma(FD<R>::a(j), col[R + h + j][e] - col[R + h - j][e], dyp[h][e]);
-            const int64_t g0 = (int64_t)(ys + i * TY + r) * nx + x0 + c;
+            const int64_t g0 = (int64_t)(ys + i * BH + r) * nx + x0 + c;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 double u0, u1, v0, v1;
-                ldpair<R>(su.at(st, r + h + R, c), u0, u1);
-                ldpair<R>(sv.at(st, r + h + 2 * R, c), v0, v1);
+                ldpair(su.at(st, r + h + R, c), u0, u1);
+                ldpair(sv.at(st, r + h + 2 * R, c), v0, v1);
                 const double uu[2] = {u0, u1}, vv[2] = {v0, v1};
                 double bu[2], bv[2];
 #pragma unroll
@@ -249,9 +254,9 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
                     bv[e] = combine<MODE_LF>(vv[e], 0.0, -A.sy * dyp[h][e], 0.0, A.cfB, 0.0);
                 }
                 const int64_t g = g0 + (int64_t)h * nx;
-                *reinterpret_cast<double2*>(A.A[0] + g) = make_double2(col[R + h][0], col[R + h][1]);
-                *reinterpret_cast<double2*>(A.B[1] + g) = make_double2(bu[0], bu[1]);
-                *reinterpret_cast<double2*>(A.B[2] + g) = make_double2(bv[0], bv[1]);
+                __stcs(reinterpret_cast<double2*>(A.A[0] + g), make_double2(col[R + h][0], col[R + h][1]));
+                __stcs(reinterpret_cast<double2*>(A.B[1] + g), make_double2(bu[0], bu[1]));
+                __stcs(reinterpret_cast<double2*>(A.B[2] + g), make_double2(bv[0], bv[1]));
             }
         }
         __syncwarp();
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(32 * (AC2_NW + 1), 1)
 acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A, const int ybase) {
     using L = ChainPLayout<R>;
     using G = Ac2Geom<R>;
-    constexpr int D = L::D, NW = AC2_NW;
+    constexpr int D = L::D, NW = AC2_NW, BH = G::BH;
     extern __shared__ __align__(128) double smem[];
     double* scru = smem + (size_t)D * L::STAGE;
     double* scrv = scru + L::SCR_U;
@@ -276,11 +281,11 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
     const int nx = A.nx;
     const int x0 = blockIdx.x * TX;
     const int ys = A.ylo + blockIdx.y * A.ychunk;
-    const int niter = min(A.ychunk, A.yhi - ys) / TY;
+    const int niter = min(A.ychunk, A.yhi - ys) / BH;
     // S_p x windows on the band rows: strips L2 L1 | centre (band rows = centre rows 2r..) | R1 R2
     const Cols<R, 5> spx{{-2 * R, -R, 0, TX, TX + R}, {R, R, TX, R, R},
                          {L::SPS, L::SPS + L::BS, L::SPC + 2 * R * TX, L::SPS + 2 * L::BS, L::SPS + 3 * L::BS}};
-    const Cols<R, 3> pu{{-R, 0, TX}, {R, TX, R}, {L::PU, L::PU + L::BS, L::PU + L::BS + TY * TX}};
+    const Cols<R, 3> pu{{-R, 0, TX}, {R, TX, R}, {L::PU, L::PU + L::BS, L::PU + L::BS + BH * TX}};
 
     if (tid == 0) {
         for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
@@ -296,7 +301,7 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             if (i >= D) mbar_wait(&empty[s], (uint32_t)(((i / D) - 1) & 1));
             mbar_expect_tx(&full[s], L::stage_bytes);
             double* st = smem + (size_t)s * L::STAGE;
-            const int y = ys + i * TY + ybase;
+            const int y = ys + i * BH + ybase;
             tma_load_3d(st + L::SPC, &M.s[0][4], x0, y - 2 * R, 0, &full[s]);
             tma_load_3d(st + L::SPS, &M.s[0][1], xl2, y, 0, &full[s]);
             tma_load_3d(st + L::SPS + L::BS, &M.s[0][1], xl1, y, 0, &full[s]);
@@ -310,61 +315,64 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
         return;
     }
     constexpr int NT = 32 * NW;
+    constexpr int QC = G::WA / 2;
+    constexpr int N1A = (BH / 2) * QC, N1B = (G::NRU / 2) * (TX / 2);
     for (int i = 0; i < niter; ++i) {
         const int s = i % D;
         mbar_wait(&full[s], (uint32_t)((i / D) & 1));
         const double* st = smem + (size_t)s * L::STAGE;
-        // phase 1a: A_u on the band rows x cols [-r, 64+r)
-        constexpr int QC = G::WA / 2;
-        for (int it = tid; it < (TY / 2) * QC; it += NT) {
-            const int r = 2 * (it / QC), c = -R + 2 * (it % QC);
+        // phase 1: A_u on the band rows x cols [-r, 64+r) (items [0, N1A)), then A_v on
+        // rows [-r, BH+r) x the band columns (items [N1A, N1A + N1B)), one item space
+        for (int it = tid; it < N1A + N1B; it += NT) {
+            if (it < N1A) {
+                const int r = 2 * (it / QC), c = -R + 2 * (it % QC);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                double w[2 * R + 2], dxp[2] = {0, 0};
+                for (int h = 0; h < 2; ++h) {
+                    double w[2 * R + 2], dxp[2] = {0, 0};
 #pragma unroll
-                for (int k = 0; k <= R; ++k) ldpair<R>(spx.at(st, r + h, c - R + 2 * k), w[2 * k], w[2 * k + 1]);
+                    for (int k = 0; k <= R; ++k) ldpair(spx.at(st, r + h, c - R + 2 * k), w[2 * k], w[2 * k + 1]);
+#pragma unroll
+                    for (int j = 1; j <= R; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) dxp[e] = fma(FD<R>::a(j), w[R + e + j] - w[R + e - j], dxp[e]);
+                    double p0, p1;
+                    ldpair(pu.at(st, r + h, c), p0, p1);
+                    const double pv[2] = {p0, p1};
+                    double au[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) au[e] = combine<MODE_LF>(pv[e], 0.0, -A.sx * dxp[e], 0.0, A.cfA, 0.0);
+                    *reinterpret_cast<double2*>(scru + (r + h) * G::WA + (c + R)) = make_double2(au[0], au[1]);
+                }
+            } else {
+                const int jt = it - N1A;
+                const int r = -R + 2 * (jt / (TX / 2)), c = 2 * (jt % (TX / 2));
+                double col[2 * R + 2][2], dyp[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+                for (int k = 0; k < 2 * R + 2; ++k)
+                    ldpair(st + L::SPC + (r - R + k + 2 * R) * TX + c, col[k][0], col[k][1]);
 #pragma unroll
                 for (int j = 1; j <= R; ++j)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) dxp[e] = fma(FD<R>::a(j), w[R + e + j] - w[R + e - j], dxp[e]);
-                double p0, p1;
-                ldpair<R>(pu.at(st, r + h, c), p0, p1);
-                const double pv[2] = {p0, p1};
-                double au[2];
+                    for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) au[e] = combine<MODE_LF>(pv[e], 0.0, -A.sx * dxp[e], 0.0, A.cfA, 0.0);
-                *reinterpret_cast<double2*>(scru + (r + h) * G::WA + (c + R)) = make_double2(au[0], au[1]);
-            }
-        }
-        // phase 1b: A_v on rows [-r, 16+r) x the band columns
-        for (int it = tid; it < (G::NRU / 2) * (TX / 2); it += NT) {
-            const int r = -R + 2 * (it / (TX / 2)), c = 2 * (it % (TX / 2));
-            double col[2 * R + 2][2], dyp[2][2] = {{0, 0}, {0, 0}};
+                        for (int e = 0; e < 2; ++e)
+                            dyp[h][e] = fma(FD<R>::a(j), col[R + h + j][e] - col[R + h - j][e], dyp[h][e]);
 #pragma unroll
-            for (int k = 0; k < 2 * R + 2; ++k)
-                ldpair<R>(st + L::SPC + (r - R + k + 2 * R) * TX + c, col[k][0], col[k][1]);
+                for (int h = 0; h < 2; ++h) {
+                    double p0, p1;
+                    ldpair(st + L::PV + (r + h + R) * TX + c, p0, p1);
+                    const double pv[2] = {p0, p1};
+                    double av[2];
 #pragma unroll
-            for (int j = 1; j <= R; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        dyp[h][e] = fma(FD<R>::a(j), col[R + h + j][e] - col[R + h - j][e], dyp[h][e]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                double p0, p1;
-                ldpair<R>(st + L::PV + (r + h + R) * TX + c, p0, p1);
-                const double pv[2] = {p0, p1};
-                double av[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) av[e] = combine<MODE_LF>(pv[e], 0.0, -A.sy * dyp[h][e], 0.0, A.cfA, 0.0);
-                *reinterpret_cast<double2*>(scrv + (r + h + R) * TX + c) = make_double2(av[0], av[1]);
+                    for (int e = 0; e < 2; ++e) av[e] = combine<MODE_LF>(pv[e], 0.0, -A.sy * dyp[h][e], 0.0, A.cfA, 0.0);
+                    *reinterpret_cast<double2*>(scrv + (r + h + R) * TX + c) = make_double2(av[0], av[1]);
+                }
             }
         }
         consumers_sync();
         // phase 2: B_p on the band
-        if (tid < (TY / 2) * (TX / 2)) {
-            const int r = 2 * (tid / (TX / 2)), c = 2 * (tid % (TX / 2));
+        for (int it = tid; it < (BH / 2) * (TX / 2); it += NT) {
+            const int r = 2 * (it / (TX / 2)), c = 2 * (it % (TX / 2));
             double dxu[2][2] = {{0, 0}, {0, 0}}, dyv[2][2] = {{0, 0}, {0, 0}};
             double cu[2][2];
 #pragma unroll
@@ -372,7 +380,7 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
                 double w[2 * R + 2];
 #pragma unroll
                 for (int k = 0; k <= R; ++k)
-                    ldpair<R>(scru + (r + h) * G::WA + (c - R + 2 * k + R), w[2 * k], w[2 * k + 1]);
+                    ldpair(scru + (r + h) * G::WA + (c - R + 2 * k + R), w[2 * k], w[2 * k + 1]);
                 cu[h][0] = w[R]; cu[h][1] = w[R + 1];
 #pragma unroll
                 for (int j = 1; j <= R; ++j)
@@ -381,7 +389,7 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
             }
             double col[2 * R + 2][2];
 #pragma unroll
-            for (int k = 0; k < 2 * R + 2; ++k) ldpair<R>(scrv + (r - R + k + R) * TX + c, col[k][0], col[k][1]);
+            for (int k = 0; k < 2 * R + 2; ++k) ldpair(scrv + (r - R + k + R) * TX + c, col[k][0], col[k][1]);
 #pragma unroll
             for (int j = 1; j <= R; ++j)
 #pragma unroll
@@ -389,20 +397,20 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
 #pragma unroll
                     for (int e = 0; e < 2; ++e)
                         dyv[h][e] = fma(FD<R>::a(j), col[R + h + j][e] - col[R + h - j][e], dyv[h][e]);
-            const int64_t g0 = (int64_t)(ys + i * TY + r) * nx + x0 + c;
+            const int64_t g0 = (int64_t)(ys + i * BH + r) * nx + x0 + c;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 double s0, s1;
-                ldpair<R>(st + L::SPC + (r + h + 2 * R) * TX + c, s0, s1);
+                ldpair(st + L::SPC + (r + h + 2 * R) * TX + c, s0, s1);
                 const double sp[2] = {s0, s1};
                 double bp[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e)
                     bp[e] = combine<MODE_LF>(sp[e], 0.0, -fma(A.sx, dxu[h][e], A.sy * dyv[h][e]), 0.0, A.cfB, 0.0);
                 const int64_t g = g0 + (int64_t)h * nx;
-                *reinterpret_cast<double2*>(A.A[1] + g) = make_double2(cu[h][0], cu[h][1]);
-                *reinterpret_cast<double2*>(A.A[2] + g) = make_double2(col[R + h][0], col[R + h][1]);
-                *reinterpret_cast<double2*>(A.B[0] + g) = make_double2(bp[0], bp[1]);
+                __stcs(reinterpret_cast<double2*>(A.A[1] + g), make_double2(cu[h][0], cu[h][1]));
+                __stcs(reinterpret_cast<double2*>(A.A[2] + g), make_double2(col[R + h][0], col[R + h][1]));
+                __stcs(reinterpret_cast<double2*>(A.B[0] + g), make_double2(bp[0], bp[1]));
             }
         }
         __syncwarp();

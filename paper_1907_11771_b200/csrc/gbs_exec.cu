@@ -12,6 +12,7 @@
 // gbs_advance replays the macro step as a CUDA graph.
 #include "gbs_internal.h"
 #include "gbs_wave3d_tma.cuh"     // substep modes and the TMA tile (no launches here)
+#include "gbs_acoustic2d_pair.cuh"  // AC2_BH (band rows of the 2-D chain kernels)
 
 // ---------------------------------------------------------------------------
 // halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
@@ -91,15 +92,17 @@ int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev) {
 // halo exchange runs on the context's comm stream while the interior planes are computed
 // on the context stream, and the two face bands follow once the exchange is in (event
 // fork / join, also inside the captured graph).  B = the face band thickness.
-static int64_t face_band(const gbs_ctx* c, const Slab& s) {
+// `rows` > 0: the launch works in bands of that many rows (the 2-D chain kernels).
+static int64_t face_band(const gbs_ctx* c, const Slab& s, int64_t rows) {
+    if (rows > 0) return rows;
     if (c->pde == GBS_ACOUSTIC2D && c->use_bulk && s.tma_ok) return gbs::tma::TY;   // whole 16-row bands
     return c->R;
 }
 
-static bool overlap_halo(gbs_ctx* c) {
+static bool overlap_halo(gbs_ctx* c, int64_t rows) {
     if (c->ghost == 0 || !c->use_overlap || c->slabs * c->loopback == 1) return false;
     for (const auto& s : c->slab)
-        if (s.nz < 3 * face_band(c, s)) return false;
+        if (s.nz < 3 * face_band(c, s, rows)) return false;
     return true;
 }
 
@@ -122,7 +125,7 @@ static int comm_join(gbs_ctx* c) {
 
 template <typename Launch>
 static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pair<int, unsigned>>& halos,
-                          bool self_ghosts = false) {
+                          bool self_ghosts = false, int64_t rows = 0) {
     int rc;
     if (c->ghost > 0 && c->slabs * c->loopback == 1) {
         // one slab with ghost rows (2-D TMA grids): only launches that read beyond the
@@ -130,7 +133,7 @@ static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pa
         if (self_ghosts && (rc = launch_ghost_fill(c, halos))) return rc;
         return launch(c->slab[0], (int64_t)0, c->slab[0].nz);
     }
-    if (!overlap_halo(c)) {
+    if (!overlap_halo(c, rows)) {
         for (auto& h : halos)
             if ((rc = exchange_halo(c, h.first, h.second))) return rc;
         for (auto& s : c->slab)
@@ -141,12 +144,12 @@ static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pa
     for (auto& h : halos)
         if ((rc = exchange_halo(c, h.first, h.second, c->cstream))) return rc;
     for (auto& s : c->slab) {
-        const int64_t B = face_band(c, s);
+        const int64_t B = face_band(c, s, rows);
         if ((rc = launch(s, B, s.nz - B))) return rc;                  // interior: no ghosts read
     }
     if ((rc = comm_join(c))) return rc;
     for (auto& s : c->slab) {
-        const int64_t B = face_band(c, s);
+        const int64_t B = face_band(c, s, rows);
         if ((rc = launch(s, (int64_t)0, B))) return rc;
         if ((rc = launch(s, s.nz - B, s.nz))) return rc;
     }
@@ -184,7 +187,7 @@ static int ac2d_pair_step(gbs_ctx* c, int cls, int P, int S, int Aout, int Bout,
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
     rc = run_overlapped(
         c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_ac2d_pair(c, s, P, S, Aout, Bout, cfA, cfB, lo, hi); },
-        {{S, 0x7u}, {P, 0x5u}}, true);
+        {{S, 0x7u}, {P, 0x5u}}, true, gbs::tma::AC2_BH);
     if (rc) return rc;
     if (end) CU(c, cudaEventRecord(end, c->stream));
     return GBS_OK;
@@ -221,7 +224,9 @@ static int enqueue_macro(gbs_ctx* c, double H) {
     int rc;
     bool first = true;
     const bool fused = fused_path(c) && c->pde == GBS_WAVE3D;
-    const bool fused2d = fused_path(c) && c->use_fuse2d && c->pde == GBS_ACOUSTIC2D;
+    bool fused2d = fused_path(c) && c->use_fuse2d && c->pde == GBS_ACOUSTIC2D;
+    for (const auto& s : c->slab)                  // the chain kernels work in whole 32-row bands
+        if (s.nz % gbs::tma::AC2_BH) fused2d = false;
     for (size_t q = 0; q < c->my_seq.size(); ++q) {
         const int k = c->my_seq[q];
         const int n = c->nk_all[k];

@@ -59,7 +59,7 @@ struct Slab {
     bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
     // [buffer][field][box]: 64x16, 64xr, rx16 (all TMA kernels); 2-D two-substep kernels also
     // 64x(16+2r), rx(16+2r), 64x(16+4r), rx(16+4r)
-    CUtensorMap tm[6][3][7];
+    CUtensorMap tm[6][3][9];
 };
 
 constexpr int kClusterMaxN = 7000;     // 4 nx doubles of shared memory per CTA

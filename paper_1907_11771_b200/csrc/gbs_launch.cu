@@ -115,11 +115,15 @@ int ensure_buffers(gbs_ctx* c) {
                     ok = make_map(&s.tm[b][f][0], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY) &&
                          make_map(&s.tm[b][f][1], base, c->n[0], vy, vz, gbs::tma::TX, c->R) &&
                          make_map(&s.tm[b][f][2], base, c->n[0], vy, vz, c->R, gbs::tma::TY);
-                    if (ok && c->pde == GBS_ACOUSTIC2D)
-                        ok = make_map(&s.tm[b][f][3], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY + 2 * c->R) &&
-                             make_map(&s.tm[b][f][4], base, c->n[0], vy, vz, c->R, gbs::tma::TY + 2 * c->R) &&
-                             make_map(&s.tm[b][f][5], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY + 4 * c->R) &&
-                             make_map(&s.tm[b][f][6], base, c->n[0], vy, vz, c->R, gbs::tma::TY + 4 * c->R);
+                    if (ok && c->pde == GBS_ACOUSTIC2D) {   // the chain kernels' boxes (Ac2PairMaps)
+                        const int BH = gbs::tma::AC2_BH;
+                        ok = make_map(&s.tm[b][f][3], base, c->n[0], vy, vz, gbs::tma::TX, BH) &&
+                             make_map(&s.tm[b][f][4], base, c->n[0], vy, vz, c->R, BH) &&
+                             make_map(&s.tm[b][f][5], base, c->n[0], vy, vz, gbs::tma::TX, BH + 2 * c->R) &&
+                             make_map(&s.tm[b][f][6], base, c->n[0], vy, vz, c->R, BH + 2 * c->R) &&
+                             make_map(&s.tm[b][f][7], base, c->n[0], vy, vz, gbs::tma::TX, BH + 4 * c->R) &&
+                             make_map(&s.tm[b][f][8], base, c->n[0], vy, vz, c->R, BH + 4 * c->R);
+                    }
                 }
             s.tma_ok = ok;
         }
@@ -186,8 +190,7 @@ static cudaError_t launch_ac2d_tma(const gbs::tma::AcMaps& m, const gbs::Acousti
 }
 // rows per CTA of the 2-D TMA kernel: a multiple of the tile height minimising
 // (waves of one-CTA-per-SM) x (rows + ~2 tiles of pipeline fill)
-static int ac2d_ychunk(int64_t xtiles, int64_t ny, int opt, int sms) {
-    const int T = gbs::tma::TY;
+static int ac2d_ychunk(int64_t xtiles, int64_t ny, int opt, int sms, int T = gbs::tma::TY) {
     if (opt > 0) return (int)std::min<int64_t>(ny, ((opt + T - 1) / T) * T);
     int64_t best = -1, bestc = T;
     for (int64_t yc = T; yc <= ny; yc += T) {
@@ -472,10 +475,10 @@ int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, doub
     a.sx = c->n[0] / c->len[0]; a.sy = c->n[1] / c->len[1];
     a.cfA = cfA; a.cfB = cfB;
     const int64_t xt = c->n[0] / gbs::tma::TX;
-    a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms);
+    a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms, gbs::tma::AC2_BH);
     dim3 grid((unsigned)xt, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
     gbs::tma::Ac2PairMaps m;
-    static const int pick[6] = {0, 2, 3, 4, 5, 6};      // Ac2PairMaps box order -> tm shape index
+    static const int pick[6] = {3, 4, 5, 6, 7, 8};      // Ac2PairMaps box order -> tm shape index
     for (int f = 0; f < 3; ++f)
         for (int k = 0; k < 6; ++k) {
             m.s[f][k] = s.tm[S][f][pick[k]];

@@ -151,6 +151,7 @@ def test_2d_bulk_kernel_bitwise_equals_register_kernel(torch_cuda, cfg, n):
 
 @pytest.mark.parametrize("cfg,n,opts", [("c3", (128, 64, 1), {}), ("c2", (128, 96, 1), {}),
                                         ("c3", (64, 48, 1), {}), ("c3", (192, 96, 1), {"loopback": 2}),
+                                        ("c3", (128, 192, 1), {"loopback": 2}),
                                         ("c2", (128, 96, 1), {"loopback": 3, "overlap": 0}),
                                         ("c3", (64, 32, 1), {"graph": 0})])
 def test_2d_two_substep_kernels_bitwise_equal_single_steps(torch_cuda, cfg, n, opts):
@@ -162,8 +163,13 @@ def test_2d_two_substep_kernels_bitwise_equal_single_steps(torch_cuda, cfg, n, o
     _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fuse2d=0))
     assert np.array_equal(a[0], b[0])
     # FE + LF1 + FIN single and (n-2)/2 pairs of two chain kernels: as many stencil launches
-    # as substeps, plus (single-slab grids) one ghost-row fill per pair
-    assert ia["kernel_launches"] >= ib["kernel_launches"]
+    # as substeps, plus (single-slab grids) one ghost-row fill per pair; slabs whose rows are
+    # not a multiple of the 32-row band run single substeps
+    slab_rows = n[1] // opts.get("loopback", 1)
+    if slab_rows % 32 == 0 and opts.get("loopback", 1) == 1:
+        assert ia["kernel_launches"] > ib["kernel_launches"]
+    else:
+        assert ia["kernel_launches"] >= ib["kernel_launches"]
     o = run_oracle(w, y0, counts, wd, H, 2)
     assert_parity(a[0], o[0], what=f"2-D pairs {cfg} {n} {opts}")
 

@@ -81,7 +81,11 @@ def stalls(path, top=10):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
-    hdr, data = rows[hi], rows[hi + 1:]
+    hdr, data = rows[hi], []
+    for r in rows[hi + 1:]:                 # the first kernel's table only
+        if len(r) != len(hdr) or r[0] == "Address":
+            break
+        data.append(r)
 
     def num(x):
         try:
