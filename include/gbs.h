@@ -243,6 +243,14 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *   "persistent"   1/0   1-D grids up to 7000 points with m <= 16: every macro step of
  *                        a gbs_advance in one thread-block-cluster launch (default 1)
  *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)
+ *   "band"         b     3-D TMA kernels: launch the x-y tiles in bands of b x-tiles (x fastest
+ *                        inside a band); 0 or a b that does not divide the x-tile count =
+ *                        whole rows (default 0; results do not depend on it)
+ *   "l2hint"       bits  two-substep 3-D kernel L2 policies: 1 z+R centre boxes evict_last,
+ *                        2 own-point boxes evict_first, 4 tile boxes evict_first, 8 streaming
+ *                        stores (default 11; results do not depend on it)
+ *   "l2hint_step"  bits  the same for the single-substep 3-D TMA kernel (1 = tile boxes
+ *                        evict_last; default 0)
  *   "overlap"      1/0   slabbed layouts: exchange the ghost planes on a comm stream
  *                        while the interior planes are computed, then the face bands
  *                        (default 1)  */

@@ -188,6 +188,18 @@ def test_two_substep_kernel_bitwise_equals_single_steps(torch_cuda, cfg, n):
     assert ia["kernel_launches"] == 2 * sum(1 + k // 2 for k in counts)
 
 
+@pytest.mark.parametrize("opts", [{"band": 1}, {"band": 2}, {"band": 3}, {"l2hint": 0},
+                                  {"l2hint": 15, "l2hint_step": 11}])
+def test_tile_order_and_cache_policies_do_not_change_results(torch_cuda, opts):
+    """The launch order of the 3-D TMA tiles (band; 3 does not divide the 4 x-tiles and falls
+    back to whole rows) and the L2 eviction policies move no arithmetic: bit-identical."""
+    w = reduced("c5", (256, 32, 20), macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=opts)
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={})
+    assert np.array_equal(a[0], b[0])
+
+
 @pytest.mark.parametrize("n,steps,wset,M", [((256, 1, 1), (2, 4, 6, 8), "square8", 200),
                                             ((77, 1, 1), (2, 4, 6, 8), "square8", 30),
                                             ((3000, 1, 1), tuple(range(2, 23, 2)), "GBS_8_6", 5)])
