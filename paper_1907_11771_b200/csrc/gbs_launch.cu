@@ -2,6 +2,10 @@
 // every kernel launch: the per-substep kernels (register z/y-march, TMA-pipelined
 // 3-D and 2-D, the two-substep 3-D kernel) over a plane range of a slab, and the
 // whole-run thread-block-cluster kernel for small 1-D grids (FD and spectral).
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "gbs_internal.h"
 #include "gbs_kernels.cuh"
 #include "gbs_wave3d_tma.cuh"
@@ -141,6 +145,21 @@ void free_state(gbs_ctx* c) {
     c->buffers_ready = false;
 }
 
+// Opt a kernel into its dynamic shared memory once per (device, kernel): the attribute
+// belongs to the device's context, so a process driving several devices sets it on each.
+static cudaError_t ensure_smem(const void* fn, size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({dev, fn})) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.insert({dev, fn});
+    return e;
+}
+
 template <int R, int MODE, bool SLAB>
 static void launch_wave3d(const gbs::Wave3DArgs& a, dim3 grid, bool vx2, cudaStream_t st) {
     if (vx2) gbs::wave3d_step<R, MODE, 2, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
@@ -150,13 +169,8 @@ template <int R, int MODE, bool SLAB>
 static cudaError_t launch_wave3d_tma(const gbs::tma::Maps& m, const gbs::Wave3DArgs& a, int zbase, dim3 grid,
                                      cudaStream_t st) {
     using L = gbs::tma::Layout<R, MODE>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gbs::tma::wave3d_step_tma<R, MODE, SLAB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::wave3d_step_tma<R, MODE, SLAB>), L::bytes);
+    if (e != cudaSuccess) return e;
     gbs::tma::wave3d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, zbase);
     return cudaSuccess;
 }
@@ -164,13 +178,8 @@ template <int R, int MODEB, bool SLAB>
 static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::PairArgs& a, int zbase, dim3 grid,
                                    cudaStream_t st) {
     using L = gbs::tma::PairLayout<R, MODEB>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gbs::tma::wave3d_pair_tma<R, MODEB, SLAB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::wave3d_pair_tma<R, MODEB, SLAB>), L::bytes);
+    if (e != cudaSuccess) return e;
     gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY / 2), L::bytes, st>>>(m, a, zbase);
     return cudaSuccess;
 }
@@ -178,13 +187,8 @@ template <int R, int MODE, bool SLAB>
 static cudaError_t launch_ac2d_tma(const gbs::tma::AcMaps& m, const gbs::Acoustic2DArgs& a, int ybase, dim3 grid,
                                    cudaStream_t st) {
     using L = gbs::tma::AcLayout<R, MODE>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gbs::tma::acoustic2d_step_tma<R, MODE, SLAB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::acoustic2d_step_tma<R, MODE, SLAB>), L::bytes);
+    if (e != cudaSuccess) return e;
     gbs::tma::acoustic2d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, ybase);
     return cudaSuccess;
 }
@@ -447,16 +451,9 @@ static cudaError_t launch_ac2d_chains(const gbs::tma::Ac2PairMaps& m, const gbs:
                                       dim3 grid, cudaStream_t st) {
     using LU = gbs::tma::ChainULayout<R>;
     using LP = gbs::tma::ChainPLayout<R>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gbs::tma::acoustic2d_chainU_tma<R>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LU::bytes);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(gbs::tma::acoustic2d_chainP_tma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)LP::bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::acoustic2d_chainU_tma<R>), LU::bytes);
+    if (e == cudaSuccess) e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::acoustic2d_chainP_tma<R>), LP::bytes);
+    if (e != cudaSuccess) return e;
     const dim3 block(32, gbs::tma::AC2_NW + 1);
     gbs::tma::acoustic2d_chainU_tma<R><<<grid, block, LU::bytes, st>>>(m, a, ybase);
     gbs::tma::acoustic2d_chainP_tma<R><<<grid, block, LP::bytes, st>>>(m, a, ybase);
