@@ -251,6 +251,9 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        stores (default 11; results do not depend on it)
  *   "l2hint_step"  bits  the same for the single-substep 3-D TMA kernel (1 = tile boxes
  *                        evict_last; default 0)
+ *   "loopback_nccl" 1/0  loopback slabs exchange their ghost planes with grouped ncclSend /
+ *                        ncclRecv on a one-rank communicator (the multi-GPU transfer path on one
+ *                        GPU; graphs off, as with world > 1; default 0)
  *   "overlap"      1/0   slabbed layouts: exchange the ghost planes on a comm stream
  *                        while the interior planes are computed, then the face bands
  *                        (default 1)  */

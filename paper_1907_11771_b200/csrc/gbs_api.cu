@@ -166,7 +166,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
         for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
         c->graph_H = -1.0;
     };
-    if (k == "graph") { c->use_graph = value != 0 && c->world == 1; drop_graphs(); return GBS_OK; }
+    if (k == "graph") { c->use_graph = value != 0 && c->world == 1 && !c->loop_nccl; drop_graphs(); return GBS_OK; }
     if (k == "time_kernels") { c->time_kernels = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "overlap") { c->use_overlap = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "l2hint") { c->hint_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
@@ -176,6 +176,23 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse2d") { c->use_fuse2d = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "loopback_nccl") {
+        if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback_nccl needs a single-GPU context");
+        const bool on = value != 0;
+        if (on && !c->comm_slab) {
+            auto& A = nccl::api();
+            if (!A.ok) return fail(c, GBS_E_NCCL, "libnccl.so.2 not found");
+            nccl::uid_t id;
+            int r = A.GetUniqueId(&id);
+            if (!r) r = A.CommInitRank(&c->comm_slab, 1, id, 0);
+            if (r) return fail(c, GBS_E_NCCL, "one-rank communicator: %s", A.GetErrorString(r));
+        }
+        cudaStreamSynchronize(c->stream);
+        drop_graphs();
+        c->loop_nccl = on;
+        c->use_graph = !on && c->use_graph;   // NCCL calls stay outside graphs, as with world > 1
+        return GBS_OK;
+    }
     if (k == "persistent") { c->use_persistent = value != 0; return GBS_OK; }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");

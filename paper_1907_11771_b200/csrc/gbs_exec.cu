@@ -33,6 +33,30 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st =
         fields = {0, 2};                        // acoustics: p and v cross the y slabs
     }
     const int nloc = c->loopback;
+    if (c->slabs == 1 && c->loop_nccl) {
+        // all slabs local, moved by NCCL point-to-point on a one-rank communicator (option
+        // "loopback_nccl": the multi-GPU transfer path -- grouped ncclSend / ncclRecv straight
+        // into the ghost planes, on the comm stream under overlap -- exercised on one GPU).
+        // Every operation has peer 0, and NCCL pairs sends and receives to one peer in
+        // posting order, so the receives are posted in the order of their matching sends.
+        auto& A = nccl::api();
+        NC(c, A.GroupStart());
+        for (int v = 0; v < nloc; ++v)
+            for (int f : fields) {
+                const double* base = field_ptr(c, c->slab[v], b, f);
+                NC(c, A.Send(base + (c->slab[v].nz - G) * P, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));  // up
+                NC(c, A.Send(base, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));                           // down
+            }
+        for (int v = 0; v < nloc; ++v)
+            for (int f : fields) {
+                Slab& up = c->slab[(v + 1) % nloc];
+                Slab& dn = c->slab[(v - 1 + nloc) % nloc];
+                NC(c, A.Recv(field_ptr(c, up, b, f) - G * P, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));
+                NC(c, A.Recv(field_ptr(c, dn, b, f) + dn.nz * P, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));
+            }
+        NC(c, A.GroupEnd());
+        return GBS_OK;
+    }
     if (c->slabs == 1) {
         // all slabs local: device-to-device copies
         for (int v = 0; v < nloc; ++v) {

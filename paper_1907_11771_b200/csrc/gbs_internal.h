@@ -129,6 +129,7 @@ struct gbs_ctx {
     int zchunk_opt = 0;
     int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
     int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
+    bool loop_nccl = false;           // loopback halos through NCCL on a one-rank communicator
     int band_opt = 0;                 // 3-D TMA tile launch order (0 = whole rows)
     int sms = 148;                    // streaming multiprocessors of the device
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};

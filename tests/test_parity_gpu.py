@@ -466,6 +466,23 @@ def test_halo_overlap_is_bitwise_identical(torch_cuda, cfg, n, slabs):
     assert_parity(a[0], o[0], what=f"overlap {cfg} {slabs} slabs")
 
 
+@pytest.mark.parametrize("cfg,n,slabs,overlap", [("c4", (64, 32, 48), 2, 1), ("c5", (64, 48, 60), 3, 1),
+                                                 ("c4", (40, 36, 36), 3, 0), ("c5", (64, 16, 24), 2, 0),
+                                                 ("c3", (200, 72, 1), 3, 1), ("c2", (128, 96, 1), 2, 0)])
+def test_loopback_halos_through_nccl(torch_cuda, cfg, n, slabs, overlap):
+    """The multi-GPU transfer path on one GPU: the loopback slabs' ghost planes move by grouped
+    ncclSend / ncclRecv on a one-rank communicator (option loopback_nccl; eager launches, halo
+    on the comm stream under overlap) -- the same bytes as the device-copy loopback."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2,
+                       opts={"loopback": slabs, "overlap": overlap, "loopback_nccl": 1})
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": overlap})
+    assert np.array_equal(a[0], b[0])
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(a[0], o[0], what=f"nccl loopback {cfg} {slabs} slabs")
+
+
 # ----------------------------------------------------------------------------- errors
 def test_error_paths(torch_cuda):
     gbs = gbs_mod()
