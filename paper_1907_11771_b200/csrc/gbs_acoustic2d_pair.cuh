@@ -93,6 +93,7 @@ struct Ac2PairArgs {
     double* B[3];            // y_{n+2}
     int nx, ny;              // ny = local slab rows
     int ylo, yhi, ychunk;    // rows [ylo, yhi) of the slab, ychunk rows per CTA (multiples of BH)
+    int yskip;               // rows skipped after the first chunk (both face bands in one launch)
     double sx, sy, cfA, cfB;
 };
 
@@ -132,7 +133,7 @@ acoustic2d_chainU_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
     const int tid = threadIdx.x + 32 * threadIdx.y, warp = threadIdx.y, lane = threadIdx.x;
     const int nx = A.nx;
     const int x0 = blockIdx.x * TX;
-    const int ys = A.ylo + blockIdx.y * A.ychunk;
+    const int ys = A.ylo + blockIdx.y * A.ychunk + (blockIdx.y ? A.yskip : 0);
     const int niter = min(A.ychunk, A.yhi - ys) / BH;
     const Cols<R, 5> su{{-2 * R, -R, 0, TX, TX + R}, {R, R, TX, R, R},
                         {L::SU, L::SU + L::BU, L::SU + 2 * L::BU, L::SU + 2 * L::BU + L::CU, L::SU + 3 * L::BU + L::CU}};
@@ -280,7 +281,7 @@ acoustic2d_chainP_tma(const __grid_constant__ Ac2PairMaps M, const Ac2PairArgs A
     const int tid = threadIdx.x + 32 * threadIdx.y, warp = threadIdx.y, lane = threadIdx.x;
     const int nx = A.nx;
     const int x0 = blockIdx.x * TX;
-    const int ys = A.ylo + blockIdx.y * A.ychunk;
+    const int ys = A.ylo + blockIdx.y * A.ychunk + (blockIdx.y ? A.yskip : 0);
     const int niter = min(A.ychunk, A.yhi - ys) / BH;
     // S_p x windows on the band rows: strips L2 L1 | centre (band rows = centre rows 2r..) | R1 R2
     const Cols<R, 5> spx{{-2 * R, -R, 0, TX, TX + R}, {R, R, TX, R, R},

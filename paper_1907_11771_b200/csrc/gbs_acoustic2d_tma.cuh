@@ -68,7 +68,7 @@ acoustic2d_step_tma(const __grid_constant__ AcMaps M, const Acoustic2DArgs A, co
     const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
     const int nx = A.nx, ny = A.ny;
     const int x0 = blockIdx.x * TX;
-    const int ys = A.ylo + blockIdx.y * A.ychunk;
+    const int ys = A.ylo + blockIdx.y * A.ychunk + (blockIdx.y ? A.yskip : 0);
     const int niter = (min(A.ychunk, A.yhi - ys) + TY - 1) / TY;   // ylo, ychunk, yhi: multiples of TY
     auto yc = [&](int y) -> int {              // tensor y coordinate of logical row y
         if constexpr (SLAB) return y + ybase;

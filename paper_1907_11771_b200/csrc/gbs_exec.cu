@@ -155,13 +155,13 @@ static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pa
         // one slab with ghost rows (2-D TMA grids): only launches that read beyond the
         // slab (self_ghosts) need them, refreshed by one copy kernel; the rest wrap
         if (self_ghosts && (rc = launch_ghost_fill(c, halos))) return rc;
-        return launch(c->slab[0], (int64_t)0, c->slab[0].nz);
+        return launch(c->slab[0], (int64_t)0, c->slab[0].nz, (int64_t)0);
     }
     if (!overlap_halo(c, rows)) {
         for (auto& h : halos)
             if ((rc = exchange_halo(c, h.first, h.second))) return rc;
         for (auto& s : c->slab)
-            if ((rc = launch(s, (int64_t)0, s.nz))) return rc;
+            if ((rc = launch(s, (int64_t)0, s.nz, (int64_t)0))) return rc;
         return GBS_OK;
     }
     if ((rc = comm_fork(c))) return rc;
@@ -169,13 +169,12 @@ static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pa
         if ((rc = exchange_halo(c, h.first, h.second, c->cstream))) return rc;
     for (auto& s : c->slab) {
         const int64_t B = face_band(c, s, rows);
-        if ((rc = launch(s, B, s.nz - B))) return rc;                  // interior: no ghosts read
+        if ((rc = launch(s, B, s.nz - B, (int64_t)0))) return rc;      // interior: no ghosts read
     }
     if ((rc = comm_join(c))) return rc;
-    for (auto& s : c->slab) {
+    for (auto& s : c->slab) {                                          // both face bands, one launch
         const int64_t B = face_band(c, s, rows);
-        if ((rc = launch(s, (int64_t)0, B))) return rc;
-        if ((rc = launch(s, s.nz - B, s.nz))) return rc;
+        if ((rc = launch(s, (int64_t)0, s.nz, s.nz - 2 * B))) return rc;
     }
     return GBS_OK;
 }
@@ -184,7 +183,7 @@ static int step(gbs_ctx* c, int cls, const StepOperands& op) {
     int rc;
     cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
-    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_step(c, s, op, lo, hi); },
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi, int64_t gap) { return launch_step(c, s, op, lo, hi, gap); },
                         {{op.S, 0u}});
     if (rc) return rc;
     if (end) CU(c, cudaEventRecord(end, c->stream));
@@ -196,7 +195,7 @@ static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
     cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
     // the pair kernel reads S_u and U with stencils
-    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_pair(c, s, op, lo, hi); },
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi, int64_t gap) { return launch_pair(c, s, op, lo, hi, gap); },
                         {{op.Su.b, 1u << op.Su.f}, {op.U.b, 1u << op.U.f}});
     if (rc) return rc;
     if (end) CU(c, cudaEventRecord(end, c->stream));
@@ -210,7 +209,10 @@ static int ac2d_pair_step(gbs_ctx* c, int cls, int P, int S, int Aout, int Bout,
     cudaEvent_t end = nullptr;
     if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
     rc = run_overlapped(
-        c, [&](Slab& s, int64_t lo, int64_t hi) { return launch_ac2d_pair(c, s, P, S, Aout, Bout, cfA, cfB, lo, hi); },
+        c,
+        [&](Slab& s, int64_t lo, int64_t hi, int64_t gap) {
+            return launch_ac2d_pair(c, s, P, S, Aout, Bout, cfA, cfB, lo, hi, gap);
+        },
         {{S, 0x7u}, {P, 0x5u}}, true, gbs::tma::AC2_BH);
     if (rc) return rc;
     if (end) CU(c, cudaEventRecord(end, c->stream));

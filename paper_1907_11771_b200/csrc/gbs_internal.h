@@ -204,13 +204,14 @@ int alloc_state(gbs_ctx* c);            // layout + flag; buffers on first use
 int ensure_buffers(gbs_ctx* c);         // allocate (or carve) the state buffers, tensor maps
 int64_t state_bytes(const gbs_ctx* c);  // device bytes of the state buffers of this layout
 void free_state(gbs_ctx* c);
-int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi);
-int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi);
+// [lo, hi) of slab s; gap > 0: only the two face bands of (hi - lo - gap) / 2 planes each
+int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi, int64_t gap = 0);
+int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi, int64_t gap = 0);
 // ghost rows of a single slab from its own opposite side, for (buffer, field mask) pairs
 int launch_ghost_fill(gbs_ctx* c, const std::vector<std::pair<int, unsigned>>& halos);
 // 2-D acoustics, two leap-frog substeps (P, S buffers -> A = y_{n+1}, B = y_{n+2} buffers)
 int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, double cfA, double cfB, int64_t lo,
-                     int64_t hi);
+                     int64_t hi, int64_t gap = 0);
 bool persistent_path(const gbs_ctx* c);
 int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);
 // ---- gbs_exec.cu

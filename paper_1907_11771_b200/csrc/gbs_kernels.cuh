@@ -112,6 +112,8 @@ struct Wave3DArgs {
     int* nonfinite;          // optional flag (FIN modes)
     double* Xu;              // optional (FE, TMA kernel): u_2 = S_u + cf2 * v_1, the first
     double cf2;              // leap-frog step's u-component, for the two-substep kernel
+    int zskip;               // planes skipped after the first z-chunk (the two face bands of a
+                             // slab in one launch); 0 = contiguous chunks
     int band;                // TMA kernels: launch order of the x-y tiles (tma::tile_of)
     int hint;                // TMA kernel L2 policy bits: 1 u tiles evict_last, 2 pointwise
                              // boxes evict_first, 8 streaming (.cs) stores
@@ -133,7 +135,7 @@ wave3d_step(const Wave3DArgs A) {
     const int tx = threadIdx.x, ty = threadIdx.y, t = ty * 32 + tx;
     const int nx = A.nx, ny = A.ny, nz = A.nz;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = A.zlo + blockIdx.z * A.zchunk;
+    const int z0 = A.zlo + blockIdx.z * A.zchunk + (blockIdx.z ? A.zskip : 0);
     const int z1 = min(z0 + A.zchunk, A.zhi);
     const int64_t plane = A.plane;
 
@@ -257,6 +259,7 @@ struct Acoustic2DArgs {
     int nx, ny;              // local extents (ny = local slab thickness)
     int ychunk;
     int ylo, yhi;            // rows [ylo, yhi) of the slab this launch computes
+    int yskip;               // rows skipped after the first y-chunk (both face bands in one launch)
     double sx, sy;           // inverse spacings
     double cf, wh;
     int* nonfinite;
@@ -275,7 +278,7 @@ acoustic2d_step(const Acoustic2DArgs A) {
     const int tx = threadIdx.x;
     const int nx = A.nx, ny = A.ny;
     const int x0 = blockIdx.x * TX;
-    const int ys = A.ylo + blockIdx.y * A.ychunk;
+    const int ys = A.ylo + blockIdx.y * A.ychunk + (blockIdx.y ? A.yskip : 0);
     const int ye = min(ys + A.ychunk, A.yhi);
     const int gx = wrap_any(x0 + tx * VX, nx);
     const bool valid = x0 + tx * VX < nx;

@@ -217,6 +217,15 @@ static int tile_band(const gbs_ctx* c, int64_t ntx) {
     return (b > 0 && ntx % b == 0) ? b : (int)ntx;
 }
 
+// gap > 0: the launch covers the two face bands [lo, lo + B) and [hi - B, hi) of a slab,
+// B = (hi - lo - gap) / 2, as two chunks of B planes (rows) with `gap` skipped between them
+static void face_chunks(int64_t lo, int64_t hi, int64_t gap, int& chunk, int& skip, unsigned& nchunks) {
+    if (gap <= 0) { skip = 0; return; }
+    chunk = (int)((hi - lo - gap) / 2);
+    skip = (int)gap;
+    nchunks = 2;
+}
+
 static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
     if (zchunk_opt > 0) return (int)std::min<int64_t>(zchunk_opt, extent);
     // aim at >= ~16 resident waves of CTAs so the tail stays small, with
@@ -228,7 +237,7 @@ static int chunk_for(int64_t tiles, int64_t extent, int zchunk_opt) {
 }
 
 // one substep over the planes [lo, hi) of slab s (lo = 0, hi = s.nz: the whole slab)
-int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi) {
+int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi, int64_t gap) {
     // slab kernels read ghost planes refreshed from neighbours; one slab (2-D TMA grids keep
     // ghost rows for the two-substep kernels) wraps periodically like a plain grid
     const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
@@ -254,6 +263,7 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
             a.band = tile_band(c, tx);
             a.hint = c->hint_step_opt;
             dim3 grid((unsigned)(tx * ty), 1u, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+            face_chunks(lo, hi, gap, a.zchunk, a.zskip, grid.z);
             gbs::tma::Maps m;
             m.su_a = s.tm[op.S][0][0]; m.su_b = s.tm[op.S][0][1]; m.su_c = s.tm[op.S][0][2];
             m.sv = s.tm[op.S][1][0];
@@ -282,6 +292,7 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
         a.zlo = (int)lo; a.zhi = (int)hi;
         a.zchunk = chunk_for(tx * ty, hi - lo, c->zchunk_opt);
         dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+        face_chunks(lo, hi, gap, a.zchunk, a.zskip, grid.z);
 #define W3(RR, SL)                                                                   \
         switch (op.mode) {                                                           \
             case gbs::MODE_FE: launch_wave3d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
@@ -293,7 +304,7 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
         else { if (slab) { W3(4, true) } else { W3(4, false) } }
 #undef W3
     } else if (c->pde == GBS_ACOUSTIC2D) {
-        gbs::Acoustic2DArgs a;
+        gbs::Acoustic2DArgs a{};
         for (int f = 0; f < 3; ++f) {
             a.S[f] = field_ptr(c, s, op.S, f);
             a.P[f] = field_ptr(c, s, op.P, f);
@@ -307,6 +318,7 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
             a.ylo = (int)lo; a.yhi = (int)hi;
             a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms);
             dim3 grid((unsigned)xt, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
+            face_chunks(lo, hi, gap, a.ychunk, a.yskip, grid.y);
             gbs::tma::AcMaps m;
             for (int f = 0; f < 3; ++f) {
                 m.s_a[f] = s.tm[op.S][f][0]; m.s_b[f] = s.tm[op.S][f][1]; m.s_c[f] = s.tm[op.S][f][2];
@@ -337,6 +349,7 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
         a.ylo = (int)lo; a.yhi = (int)hi;
         a.ychunk = chunk_for(tx, hi - lo, c->zchunk_opt);
         dim3 grid((unsigned)tx, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
+        face_chunks(lo, hi, gap, a.ychunk, a.yskip, grid.y);
 #define A2(RR, SL)                                                                   \
         switch (op.mode) {                                                           \
             case gbs::MODE_FE: launch_ac2d<RR, gbs::MODE_FE, SL>(a, grid, vx2, c->stream); break;   \
@@ -370,12 +383,12 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
     return GBS_OK;
 }
 
-int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi) {
+int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi, int64_t gap) {
     // slab kernels read ghost planes refreshed from neighbours; one slab (2-D TMA grids keep
     // ghost rows for the two-substep kernels) wraps periodically like a plain grid
     const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
     const bool lf = op.modeB == gbs::MODE_LF;
-    gbs::tma::PairArgs a;
+    gbs::tma::PairArgs a{};
     if (lf) {
         a.Av = field_ptr(c, s, op.Av.b, op.Av.f);
         a.Bu = field_ptr(c, s, op.Bu.b, op.Bu.f); a.Bv = field_ptr(c, s, op.Bv.b, op.Bv.f);
@@ -398,6 +411,7 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     a.hint = c->hint_opt;
     dim3 grid((unsigned)((c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY)), 1u,
               (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+    face_chunks(lo, hi, gap, a.zchunk, a.zskip, grid.z);
     gbs::tma::PairMaps m;
     m.su_a = s.tm[op.Su.b][op.Su.f][0]; m.su_b = s.tm[op.Su.b][op.Su.f][1]; m.su_c = s.tm[op.Su.b][op.Su.f][2];
     m.u_a = s.tm[op.U.b][op.U.f][0]; m.u_b = s.tm[op.U.b][op.U.f][1]; m.u_c = s.tm[op.U.b][op.U.f][2];
@@ -461,8 +475,8 @@ static cudaError_t launch_ac2d_chains(const gbs::tma::Ac2PairMaps& m, const gbs:
 }
 
 int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, double cfA, double cfB, int64_t lo,
-                     int64_t hi) {
-    gbs::tma::Ac2PairArgs a;
+                     int64_t hi, int64_t gap) {
+    gbs::tma::Ac2PairArgs a{};
     for (int f = 0; f < 3; ++f) {
         a.A[f] = field_ptr(c, s, Aout, f);
         a.B[f] = field_ptr(c, s, Bout, f);
@@ -474,6 +488,7 @@ int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, doub
     const int64_t xt = c->n[0] / gbs::tma::TX;
     a.ychunk = ac2d_ychunk(xt, hi - lo, c->zchunk_opt, c->sms, gbs::tma::AC2_BH);
     dim3 grid((unsigned)xt, (unsigned)((hi - lo + a.ychunk - 1) / a.ychunk));
+    face_chunks(lo, hi, gap, a.ychunk, a.yskip, grid.y);
     gbs::tma::Ac2PairMaps m;
     static const int pick[6] = {3, 4, 5, 6, 7, 8};      // Ac2PairMaps box order -> tm shape index
     for (int f = 0; f < 3; ++f)

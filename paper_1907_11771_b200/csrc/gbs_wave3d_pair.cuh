@@ -74,6 +74,7 @@ struct PairArgs {
     const double* Su; const double* U;
     int nx, ny, nz, zchunk;
     int zlo, zhi;                     // planes [zlo, zhi) of the slab this launch computes
+    int zskip;                        // planes skipped after the first chunk (Wave3DArgs::zskip)
     int64_t plane;
     double sx2, sy2, sz2;
     double cfA, cfB, wh;
@@ -100,7 +101,7 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     int xt, yt;
     tile_of(blockIdx.x, nx / TX, ny / TY, A.band, xt, yt);
     const int x0 = xt * TX, y0 = yt * TY;
-    const int z0 = A.zlo + blockIdx.z * A.zchunk;
+    const int z0 = A.zlo + blockIdx.z * A.zchunk + (blockIdx.z ? A.zskip : 0);
     const int niter = min(A.zchunk, A.zhi - z0);
     auto zc = [&](int z) -> int {
         if constexpr (SLAB) return z + zbase;

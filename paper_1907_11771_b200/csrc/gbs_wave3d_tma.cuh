@@ -144,7 +144,7 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
     int xt, yt;
     tile_of(blockIdx.x, nx / TX, ny / TY, A.band, xt, yt);
     const int x0 = xt * TX, y0 = yt * TY;
-    const int z0 = A.zlo + blockIdx.z * A.zchunk;
+    const int z0 = A.zlo + blockIdx.z * A.zchunk + (blockIdx.z ? A.zskip : 0);
     const int niter = min(A.zchunk, A.zhi - z0);
 
     auto zc = [&](int z) -> int {              // tensor z coordinate of logical plane z
