@@ -57,8 +57,8 @@ struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
     double* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // Y, ACC, L0..L3 (+ ghosts)
     bool tma_ok = false;              // tensor maps below are valid (TMA kernels eligible)
-    // [buffer][field][box]: 64x16, 64xr, rx16 (all TMA kernels); 2-D two-substep kernels also
-    // 64x(16+2r), rx(16+2r), 64x(16+4r), rx(16+4r)
+    // [buffer][field][box]: 64x16, 64xr, rx16 (all TMA kernels); the 2-D chain kernels also
+    // 64xBH, rxBH, 64x(BH+2r), rx(BH+2r), 64x(BH+4r), rx(BH+4r) (BH = tma::AC2_BH = 32 rows)
     CUtensorMap tm[6][3][9];
 };
 

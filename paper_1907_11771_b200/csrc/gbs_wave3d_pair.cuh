@@ -34,6 +34,10 @@
 // that carry the z stencils), and the own-point boxes S_v, P_v (and the
 // accumulator) of plane z.  D = 3 stages (the two-stage version waited on the
 // TMA barrier ~23% of the time, profiles/r01_ncu_pair_c5_src.txt).
+// L2 policies (PairArgs::hint, default 11): the z+R centre boxes are loaded
+// evict_last (re-read R planes later as the tile centre), the own-point boxes
+// evict_first, and the outputs are streaming stores -- 10% fewer DRAM reads
+// (profiles/r01_ncu_pair6_c5.txt).
 #pragma once
 
 #include "gbs_wave3d_tma.cuh"
