@@ -202,6 +202,10 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
             double xw[2 * R + 2];
 #pragma unroll
             for (int k = 0; k <= R; ++k) {
+                if (k == R / 2) {                   // the thread's own points: already in the queue
+                    xw[2 * k] = q[R][2 * r]; xw[2 * k + 1] = q[R][2 * r + 1];
+                    continue;
+                }
                 const double2 a = *reinterpret_cast<const double2*>(tile + woff[r][k]);
                 xw[2 * k] = a.x; xw[2 * k + 1] = a.y;
             }

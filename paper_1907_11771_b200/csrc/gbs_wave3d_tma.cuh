@@ -235,6 +235,10 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
         double xw[2 * R + 2];
 #pragma unroll
         for (int k = 0; k <= R; ++k) {
+            if (k == R / 2) {                   // the thread's own points: already in the queue
+                xw[2 * k] = q[R].v[0]; xw[2 * k + 1] = q[R].v[1];
+                continue;
+            }
             const int col = 2 * tx - R + 2 * k;
             const double* src = col < 0 ? tile + L::CENTER + ty * R + (col + R)
                               : col >= TX ? tile + L::CENTER + L::STRIP + ty * R + (col - TX)
