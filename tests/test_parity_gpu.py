@@ -644,3 +644,46 @@ def test_3d_full_size_sampled(torch_cuda, cfg):
     scale = np.sqrt(np.mean(y0 * y0))          # RMS of the input (|R| <= 1: norms do not grow)
     err = np.max(np.abs(got - ref)) / scale
     assert err <= TOL, f"{cfg}: max |gpu - oracle| / rms = {err:.3e}"
+
+
+# ----------------------------------------------------------------------------- randomized
+def _random_cases(seed=20261020, count=14):
+    """Seeded random small cases: PDE, grid (TMA-sized or ragged), slab count and options.
+    Every case is checked against the oracle, so a bug in any launch variant (register / TMA /
+    two-substep kernels, slabs, overlap split, face-band launch, graphs, tile order) shows."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    while len(cases) < count:
+        cfg = str(rng.choice(["c2", "c3", "c4", "c5"]))
+        if cfg in ("c4", "c5"):
+            nx = int(rng.choice([64, 128, 40, 72]))
+            ny = int(rng.choice([16, 32, 36]))
+            nz = int(rng.choice([16, 24, 30, 48]))
+            n = (nx, ny, nz)
+            slow = nz
+        else:
+            nx = int(rng.choice([64, 128, 96, 200]))
+            ny = int(rng.choice([32, 48, 64, 96, 72]))
+            n = (nx, ny, 1)
+            slow = ny
+        R = 4 if cfg in ("c3", "c4", "c5") else 2
+        lbs = [s for s in (1, 2, 3, 4) if slow % s == 0 and slow // s >= R]
+        lb = int(rng.choice(lbs))
+        opts = {"loopback": lb, "overlap": int(rng.integers(0, 2)), "graph": int(rng.integers(0, 2)),
+                "fuse": int(rng.integers(0, 2)), "band": int(rng.choice([0, 1, 2])),
+                "zchunk": int(rng.choice([0, 0, 8, 17]))}
+        if cfg in ("c2", "c3"):
+            opts["fuse2d"] = int(rng.integers(0, 2))
+        if lb > 1 and rng.integers(0, 4) == 0:
+            opts["loopback_nccl"] = 1
+        cases.append((cfg, n, opts))
+    return cases
+
+
+@pytest.mark.parametrize("cfg,n,opts", _random_cases())
+def test_randomized_launch_variants_match_oracle(torch_cuda, cfg, n, opts):
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=opts)
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(g[0], o[0], what=f"{cfg} {n} {opts}")
