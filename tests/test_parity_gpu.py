@@ -647,14 +647,18 @@ def test_3d_full_size_sampled(torch_cuda, cfg):
 
 
 # ----------------------------------------------------------------------------- randomized
-def _random_cases(seed=20261020, count=14):
+def _random_cases(seed=20261020, count=14, include_1d=False):
     """Seeded random small cases: PDE, grid (TMA-sized or ragged), slab count and options.
     Every case is checked against the oracle, so a bug in any launch variant (register / TMA /
     two-substep kernels, slabs, overlap split, face-band launch, graphs, tile order) shows."""
     rng = np.random.default_rng(seed)
     cases = []
     while len(cases) < count:
-        cfg = str(rng.choice(["c2", "c3", "c4", "c5"]))
+        cfg = str(rng.choice(["c1", "c2", "c3", "c4", "c5"] if include_1d else ["c2", "c3", "c4", "c5"]))
+        if cfg == "c1":
+            cases.append((cfg, (int(rng.integers(9, 700)), 1, 1),
+                          {"persistent": int(rng.integers(0, 2)), "graph": int(rng.integers(0, 2))}))
+            continue
         if cfg in ("c4", "c5"):
             nx = int(rng.choice([64, 128, 40, 72]))
             ny = int(rng.choice([16, 32, 36]))
@@ -682,8 +686,9 @@ def _random_cases(seed=20261020, count=14):
 
 @pytest.mark.parametrize("cfg,n,opts", _random_cases())
 def test_randomized_launch_variants_match_oracle(torch_cuda, cfg, n, opts):
-    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
-    counts, wd, H = scheme_for(w, "nonzero8")
+    wset = "square8" if cfg == "c1" else "nonzero8"
+    w = reduced(cfg, n, macro_steps=2, weights=wset)
+    counts, wd, H = scheme_for(w, wset)
     y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=opts)
     o = run_oracle(w, y0, counts, wd, H, 2)
     assert_parity(g[0], o[0], what=f"{cfg} {n} {opts}")

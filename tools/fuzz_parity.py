@@ -21,10 +21,11 @@ gbs.load()
 seed = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 bad = 0
-for cfg, n, opts in tp._random_cases(seed, count):
+for cfg, n, opts in tp._random_cases(seed, count, include_1d=True):
     try:
-        w = tp.reduced(cfg, n, macro_steps=2, weights="nonzero8")
-        counts, wd, H = tp.scheme_for(w, "nonzero8")
+        wset = "square8" if cfg == "c1" else "nonzero8"
+        w = tp.reduced(cfg, n, macro_steps=2, weights=wset)
+        counts, wd, H = tp.scheme_for(w, wset)
         y0, g, _ = tp.run_gpu(torch, w, counts, wd, H, 2, opts=opts)
         o = tp.run_oracle(w, y0, counts, wd, H, 2)
         tp.assert_parity(g[0], o[0], what=f"{cfg} {n} {opts}")
