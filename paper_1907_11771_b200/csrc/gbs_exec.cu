@@ -171,12 +171,17 @@ static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pa
         const int64_t B = face_band(c, s, rows);
         if ((rc = launch(s, B, s.nz - B, (int64_t)0))) return rc;      // interior: no ghosts read
     }
-    if ((rc = comm_join(c))) return rc;
-    for (auto& s : c->slab) {                                          // both face bands, one launch
+    // both face bands in one launch, queued on the comm stream behind the exchange: it starts
+    // as soon as the ghosts are in and fills the SMs the interior launch's last wave leaves
+    // idle (the two launches write disjoint planes; every in-place read is pointwise)
+    std::swap(c->stream, c->cstream);                 // the launchers enqueue on c->stream
+    for (auto& s : c->slab) {
         const int64_t B = face_band(c, s, rows);
-        if ((rc = launch(s, (int64_t)0, s.nz, s.nz - 2 * B))) return rc;
+        if ((rc = launch(s, (int64_t)0, s.nz, s.nz - 2 * B))) break;
     }
-    return GBS_OK;
+    std::swap(c->stream, c->cstream);
+    if (rc) return rc;
+    return comm_join(c);
 }
 
 static int step(gbs_ctx* c, int cls, const StepOperands& op) {
