@@ -312,7 +312,7 @@ def run_ours(a):
         clk.start()
         t_ms = timed(a.steps)
         barrier()
-        clocks = clk.stop()
+        clocks = pdist.merge_clocks(pdist.gather_objects(clk.stop()))
         gbs.gbs_sync(st.ctx)
         ms = max_over_ranks(t_ms)
         launches = st.info()["kernel_launches"] - l0

@@ -64,3 +64,26 @@ def sum_over_ranks(x: float, device: Optional[torch.device] = None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device or "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def gather_objects(obj):
+    """Every rank's picklable `obj`, in rank order (a one-element list on one process)."""
+    if not active():
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def merge_clocks(per_rank):
+    """One clocks record for a multi-GPU timed region from every rank's sampler output:
+    the lowest per-rank median SM clock (the slowest GPU sets the max-over-ranks time), the
+    union of throttle reasons, and each rank's own record."""
+    if len(per_rank) == 1:
+        return per_rank[0]
+    sm = [c.get("sm_mhz") for c in per_rank if c.get("sm_mhz") is not None]
+    mx = [c.get("sm_max_mhz") for c in per_rank if c.get("sm_max_mhz") is not None]
+    reasons = sorted({r for c in per_rank for r in c.get("reasons", [])})
+    return {"sm_mhz": min(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+            "reasons": reasons, "samples": sum(int(c.get("samples", 0)) for c in per_rank),
+            "per_rank": per_rank}

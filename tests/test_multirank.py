@@ -182,6 +182,13 @@ def _helpers_worker(rank, world):
     pdist.barrier(sync_cuda=False)
     assert pdist.max_over_ranks(10.0 + rank) == 10.0 + world - 1
     assert pdist.sum_over_ranks(1.0) == world
+    got = pdist.gather_objects({"rank": rank})
+    assert [g["rank"] for g in got] == list(range(world))
+    recs = pdist.gather_objects({"sm_mhz": 1500.0 + rank, "sm_max_mhz": 1965.0,
+                                 "reasons": ["sw_power_cap"] if rank == 1 else [], "samples": 2})
+    m = pdist.merge_clocks(recs)
+    assert m["sm_mhz"] == 1500.0 and m["reasons"] == ["sw_power_cap"] and m["samples"] == 2 * world
+    assert len(m["per_rank"]) == world
 
 
 @pytest.mark.parametrize("world", [2, 4])
