@@ -315,7 +315,8 @@ def run_ours(a):
         clocks = pdist.merge_clocks(pdist.gather_objects(clk.stop()))
         gbs.gbs_sync(st.ctx)
         ms = max_over_ranks(t_ms)
-        launches = st.info()["kernel_launches"] - l0
+        launches_rank = st.info()["kernel_launches"] - l0
+        launches = int(pdist.sum_over_ranks(launches_rank))       # the whole job's launches
         # the same region again (SURVEY §8(d) timing protocol: repeat, report median and best)
         rep_ms = [ms]
         for _ in range(max(0, a.repeats - 1)):
@@ -444,6 +445,7 @@ def run_ours(a):
                            "hbm_roofline_fraction_of_step": round(
                                value * 24 * F / (peak * 1e9 * world), 4)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "gpu_launches_per_rank": launches_rank,
                 "sim_time_per_s": H * a.steps / (ms * 1e-3),
                 "repeats": {"n": len(rep_ms),
                             "values": [round(w.points * S * a.steps / (r * 1e-3), 1) for r in rep_ms],
