@@ -316,7 +316,7 @@ def run_ours(a):
         gbs.gbs_sync(st.ctx)
         ms = max_over_ranks(t_ms)
         launches_rank = st.info()["kernel_launches"] - l0
-        launches = int(pdist.sum_over_ranks(launches_rank))       # the whole job's launches
+        launches = int(pdist.sum_over_ranks(launches_rank, dev))  # the whole job's launches
         # the same region again (SURVEY §8(d) timing protocol: repeat, report median and best)
         rep_ms = [ms]
         for _ in range(max(0, a.repeats - 1)):
