@@ -154,8 +154,11 @@ GBS_API int gbs_halo_schedule(int slabs, int my_slab, int64_t nz_local, int ghos
  *   grid           problem description (copied)
  *   stencil_order  4 or 8 (centered FD, radius r = order / 2), or 0: spectral
  *                  derivative of the trigonometric interpolant (GBS_ADV1D only,
- *                  n[0] even, 4..6400, m <= 16; runs as one thread-block-cluster
- *                  launch per gbs_advance on one GPU -- GBS_E_UNSUPPORTED otherwise)
+ *                  n[0] even, >= 4).  n[0] <= 6400 with m <= 16 on one
+ *                  GPU: one thread-block-cluster launch per gbs_advance (option
+ *                  "persistent"); otherwise per substep cuFFT D2Z, i k scaling, Z2D
+ *                  and the pointwise update (libcufft.so.11 resolved at run time;
+ *                  GBS_E_UNSUPPORTED if absent)
  *   m, n_k, w_k    step counts (even, >= 2, distinct; 1 <= m <= 32) and their
  *                  fp64 weights (already rounded once from exact rationals by
  *                  the caller); both copied.  Sequences with

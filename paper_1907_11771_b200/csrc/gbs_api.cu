@@ -25,6 +25,24 @@ Api& api() {
 }
 }  // namespace nccl
 
+namespace cufft {
+Api& api() {
+    static Api a;
+    static bool tried = false;
+    if (tried) return a;
+    tried = true;
+    void* h = dlopen("libcufft.so.11", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcufft.so.11", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcufft.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+#define CUFFT_SYM(name) a.name = (decltype(a.name))dlsym(h, "cufft" #name); if (!a.name) return a;
+    CUFFT_SYM(Plan1d) CUFFT_SYM(ExecD2Z) CUFFT_SYM(ExecZ2D) CUFFT_SYM(SetStream) CUFFT_SYM(Destroy)
+#undef CUFFT_SYM
+    a.ok = true;
+    return a;
+}
+}  // namespace cufft
+
 thread_local std::string g_err;
 
 int fail(gbs_ctx* c, int code, const char* fmt, ...) {
@@ -91,6 +109,7 @@ void gbs_destroy(gbs_ctx* c) {
     if (c->d_nk) cudaFree(c->d_nk);
     if (c->d_wh) cudaFree(c->d_wh);
     if (c->d_alpha) cudaFree(c->d_alpha);
+    spectral_release(c);
     for (auto e : c->timer.ev) cudaEventDestroy(e);
     auto& A = nccl::api();
     if (A.ok) {

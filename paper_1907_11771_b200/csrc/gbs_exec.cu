@@ -350,9 +350,6 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
         c->t += H * (double)macro_steps;
         return GBS_OK;
     }
-    if (c->order == 0)
-        return fail(c, GBS_E_UNSUPPORTED, "the spectral derivative runs only in the cluster kernel "
-                                          "(one GPU, no loopback, option persistent=1)");
     const bool graph = c->use_graph && !c->time_kernels && macro_steps > 0;
     if (graph && c->graph_H != H) {
         for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }

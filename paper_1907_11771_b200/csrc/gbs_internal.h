@@ -52,6 +52,23 @@ struct Api {
 Api& api();                        // gbs_api.cu
 }  // namespace nccl
 
+namespace cufft {
+// cuFFT, resolved at run time (the process's libcufft.so.11, e.g. torch's) for the spectral
+// derivative on grids beyond the cluster kernel; plans are made once per context
+typedef int handle_t;
+enum { D2Z = 0x6a, Z2D = 0x6c };
+typedef int (*Plan1d_t)(handle_t*, int, int, int);
+typedef int (*ExecD2Z_t)(handle_t, double*, void*);
+typedef int (*ExecZ2D_t)(handle_t, void*, double*);
+typedef int (*SetStream_t)(handle_t, cudaStream_t);
+typedef int (*Destroy_t)(handle_t);
+struct Api {
+    bool ok = false;
+    Plan1d_t Plan1d; ExecD2Z_t ExecD2Z; ExecZ2D_t ExecZ2D; SetStream_t SetStream; Destroy_t Destroy;
+};
+Api& api();                        // gbs_api.cu
+}  // namespace cufft
+
 // ---------------------------------------------------------------------------
 struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
@@ -105,6 +122,8 @@ struct gbs_ctx {
     bool use_bulk = true;             // bulk-copy (TMA engine) pipelined kernels where eligible
     bool use_persistent = true;       // one cluster launch per gbs_advance for small 1-D grids
     double* d_alpha = nullptr;        // spectral derivative weights (order 0)
+    int fft_fwd = -1, fft_inv = -1;   // cuFFT D2Z / Z2D plans (order 0 beyond the cluster kernel)
+    double* fft_buf = nullptr;        // N/2 + 1 complex spectrum, then the N-point derivative
     // asynchronous slab IO (gbs_write_slab_async / gbs_read_slab_async): per local slab a
     // staging buffer for the incoming and for the outgoing state, own copy streams
     std::vector<double*> in_buf, out_buf;
@@ -213,6 +232,8 @@ int launch_ghost_fill(gbs_ctx* c, const std::vector<std::pair<int, unsigned>>& h
 int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, double cfA, double cfB, int64_t lo,
                      int64_t hi, int64_t gap = 0);
 bool persistent_path(const gbs_ctx* c);
+int spectral_setup(gbs_ctx* c);       // cuFFT plans + buffers (order 0); idempotent
+void spectral_release(gbs_ctx* c);
 int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);
 // ---- gbs_exec.cu
 int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev);

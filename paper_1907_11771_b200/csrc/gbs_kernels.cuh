@@ -399,6 +399,33 @@ struct Adv1DArgs {
     int nx; double sx; double cf, wh; int* nonfinite;
 };
 
+// Spectral derivative (order 0) on grids beyond the cluster kernel, between cuFFT's D2Z and
+// Z2D: spec[k] <- i s k spec[k] for 0 <= k < N/2 (s = 2 pi / (L N), the 1/N of the unnormalised
+// inverse included), the Nyquist coefficient dropped (it has no odd derivative)
+template <int Unused = 0>
+__global__ void __launch_bounds__(256) spectral_ik(double2* spec, int n, double s) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > n / 2) return;
+    const double2 t = spec[k];
+    const double m = s * (double)k;
+    spec[k] = (k == n / 2) ? make_double2(0.0, 0.0) : make_double2(-m * t.y, m * t.x);
+}
+
+// the pointwise update of one substep from the spectral derivative du = u_x: f = -u_x
+template <int MODE>
+__global__ void __launch_bounds__(256) adv1d_spectral_update(const Adv1DArgs A, const double* du) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= A.nx) return;
+    const double f = -du[x];
+    double p = 0.0, a = 0.0;
+    if constexpr (MODE != MODE_FE) p = A.P[x];
+    if constexpr (MODE == MODE_FINACC) a = A.O[x];
+    const double o = combine<MODE>(p, A.S[x], f, a, A.cf, A.wh);
+    A.O[x] = o;
+    if constexpr (MODE == MODE_FIN0 || MODE == MODE_FINACC)
+        if (!isfinite(o) && A.nonfinite) *A.nonfinite = 1;
+}
+
 template <int R, int MODE, int NT>
 __global__ void __launch_bounds__(NT)
 adv1d_step(const Adv1DArgs A) {

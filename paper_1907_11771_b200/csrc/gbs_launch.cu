@@ -48,7 +48,11 @@ static bool make_map(CUtensorMap* m, double* base, int64_t nx, int64_t ny, int64
 // Layout of the state: slabs of the slowest axis with ghost planes, the number of
 // buffers per slab; no device memory yet (ensure_buffers allocates on first use, from
 // a caller-bound workspace when there is one).
+static int launch_spectral_step(gbs_ctx* c, const gbs::Adv1DArgs& a, int mode);   // below
+
 int alloc_state(gbs_ctx* c) {
+    int rc0 = spectral_setup(c);     // plans before any graph capture (they allocate)
+    if (rc0) return rc0;
     int nloc = c->loopback;
     int64_t total_slabs = (int64_t)c->slabs * nloc;
     int64_t nzl = c->nslow / total_slabs;
@@ -365,6 +369,13 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
         a.S = field_ptr(c, s, op.S, 0); a.P = field_ptr(c, s, op.P, 0); a.O = field_ptr(c, s, op.O, 0);
         a.nx = (int)c->n[0]; a.sx = c->n[0] / c->len[0];
         a.cf = op.cf; a.wh = op.wh; a.nonfinite = flag;
+        if (c->order == 0) {
+            const int rc = launch_spectral_step(c, a, op.mode);
+            if (rc) return rc;
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+            return GBS_OK;
+        }
         constexpr int NT = 256;
         dim3 grid((unsigned)((c->n[0] + NT - 1) / NT));
 #define A1(RR)                                                                            \
@@ -513,7 +524,61 @@ int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, doub
 bool persistent_path(const gbs_ctx* c) {
     const int m = (int)c->my_seq.size();
     return c->use_persistent && c->pde == GBS_ADV1D && c->world == 1 && c->loopback == 1 && m >= 1 &&
-           m <= 16 && c->n[0] <= kClusterMaxN;
+           m <= 16 && c->n[0] <= (c->order == 0 ? kSpectralMaxN : kClusterMaxN);
+}
+
+// ---------------------------------------------------------------------------
+// spectral derivative beyond the cluster kernel: per substep D2Z, multiply by
+// i 2 pi k / (L N) (Nyquist dropped), Z2D -- the derivative of the trigonometric
+// interpolant (the oracle's definition, R20) -- then the
+// pointwise FE / LF / final update
+// ---------------------------------------------------------------------------
+int spectral_setup(gbs_ctx* c) {
+    if (c->order != 0 || c->fft_fwd >= 0) return GBS_OK;
+    auto& F = cufft::api();
+    if (!F.ok) return fail(c, GBS_E_UNSUPPORTED, "libcufft.so.11 not found (spectral derivative, N > %d)",
+                           kSpectralMaxN);
+    const int n = (int)c->n[0];
+    CU(c, cudaMalloc(&c->fft_buf, sizeof(double) * (size_t)(2 * (n / 2 + 1) + n)));
+    int r = F.Plan1d(&c->fft_fwd, n, cufft::D2Z, 1);
+    if (!r) r = F.Plan1d(&c->fft_inv, n, cufft::Z2D, 1);
+    if (!r) r = F.SetStream(c->fft_fwd, c->stream);
+    if (!r) r = F.SetStream(c->fft_inv, c->stream);
+    if (r) return fail(c, GBS_E_CUDA, "cuFFT plan setup failed (%d)", r);
+    return GBS_OK;
+}
+
+void spectral_release(gbs_ctx* c) {
+    auto& F = cufft::api();
+    if (F.ok) {
+        if (c->fft_fwd >= 0) F.Destroy(c->fft_fwd);
+        if (c->fft_inv >= 0) F.Destroy(c->fft_inv);
+    }
+    c->fft_fwd = c->fft_inv = -1;
+    if (c->fft_buf) cudaFree(c->fft_buf);
+    c->fft_buf = nullptr;
+}
+
+static int launch_spectral_step(gbs_ctx* c, const gbs::Adv1DArgs& a, int mode) {
+    auto& F = cufft::api();
+    const int n = a.nx;
+    double2* spec = reinterpret_cast<double2*>(c->fft_buf);
+    double* du = c->fft_buf + 2 * (n / 2 + 1);
+    int r = F.ExecD2Z(c->fft_fwd, const_cast<double*>(a.S), spec);
+    if (r) return fail(c, GBS_E_CUDA, "cufftExecD2Z failed (%d)", r);
+    const double s = 2.0 * 3.14159265358979323846 / (c->len[0] * (double)n);
+    gbs::spectral_ik<<<(unsigned)((n / 2 + 1 + 255) / 256), 256, 0, c->stream>>>(spec, n, s);
+    r = F.ExecZ2D(c->fft_inv, spec, du);
+    if (r) return fail(c, GBS_E_CUDA, "cufftExecZ2D failed (%d)", r);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    switch (mode) {
+        case gbs::MODE_FE: gbs::adv1d_spectral_update<gbs::MODE_FE><<<g, 256, 0, c->stream>>>(a, du); break;
+        case gbs::MODE_LF: gbs::adv1d_spectral_update<gbs::MODE_LF><<<g, 256, 0, c->stream>>>(a, du); break;
+        case gbs::MODE_FIN0: gbs::adv1d_spectral_update<gbs::MODE_FIN0><<<g, 256, 0, c->stream>>>(a, du); break;
+        default: gbs::adv1d_spectral_update<gbs::MODE_FINACC><<<g, 256, 0, c->stream>>>(a, du); break;
+    }
+    c->launches += 2;                                  // ours; cuFFT's own kernels not counted
+    return GBS_OK;
 }
 
 int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H) {

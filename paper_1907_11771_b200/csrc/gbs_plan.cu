@@ -126,14 +126,12 @@ int validate(gbs_ctx* c, const gbs_grid* g, int stencil_order, int m, const int3
     else return fail(c, GBS_E_INVAL, "grid.pde=%d is not a known PDE", g->pde);
     if (g->ndim != c->ndim) return fail(c, GBS_E_INVAL, "grid.ndim=%d does not match the PDE", g->ndim);
     if (stencil_order == 0) {
-        // spectral derivative: 1-D advection on an even grid, whole run in
-        // the cluster kernel (N <= kClusterMaxN, m <= 16, one GPU)
+        // spectral derivative: 1-D advection on an even grid -- the whole run
+        // in the cluster kernel (N <= kSpectralMaxN, m <= 16, one GPU), else cuFFT per substep
         if (g->pde != GBS_ADV1D)
             return fail(c, GBS_E_INVAL, "stencil_order=0 (spectral) is defined for GBS_ADV1D only");
-        if (g->n[0] < 4 || g->n[0] % 2 || g->n[0] > kSpectralMaxN)
-            return fail(c, GBS_E_INVAL, "spectral grid n[0]=%lld must be even, 4..%d", (long long)g->n[0],
-                        kSpectralMaxN);
-        if (m > 16) return fail(c, GBS_E_INVAL, "spectral runs one sequence per CTA of a cluster: m=%d > 16", m);
+        if (g->n[0] < 4 || g->n[0] % 2 || g->n[0] > (1LL << 30))
+            return fail(c, GBS_E_INVAL, "spectral grid n[0]=%lld must be even, 4..2^30", (long long)g->n[0]);
     } else if (stencil_order != 4 && stencil_order != 8) {
         return fail(c, GBS_E_INVAL, "stencil_order=%d (must be 4 or 8, or 0 = spectral)", stencil_order);
     }

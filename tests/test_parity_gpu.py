@@ -279,13 +279,43 @@ def test_spectral_section41(torch_cuda, wset, N):
     assert err_gpu <= 1.01 * err_or + 1e-13
 
 
-def test_spectral_is_cluster_only(torch_cuda):
-    gbs = gbs_mod()
-    with gbs.Stepper("adv1d", (64, 1, 1), 0, [2, 4], [-1 / 3, 4 / 3], persistent=0) as st:
-        st.write(np.ones((1, 64)))
-        with pytest.raises(gbs.GbsError) as e:
-            st.advance(1, 1e-3)
-        assert e.value.code == gbs.GBS_E_UNSUPPORTED
+@pytest.mark.parametrize("wset,N,opts", [("GBS_8_6", 64, {"persistent": 0}), ("GBS_12_8", 256, {"persistent": 0}),
+                                          ("square8", 8192, {}), ("square8", 6402, {"graph": 0})])
+def test_spectral_fft_path(torch_cuda, wset, N, opts):
+    """The spectral derivative beyond the cluster kernel (N > 6400, or option persistent=0):
+    cuFFT D2Z, multiplication by i 2 pi k (Nyquist dropped), Z2D, then the pointwise substep
+    update -- against the oracle's DFT derivative, the section 4.1 IC and H rule."""
+    import math
+    w = get_config("s41").with_(n=(N, 1, 1))
+    counts, ws, _ = W.scheme(wset)
+    wd = W.to_double(ws)
+    H = 1.0 / math.ceil(1.0 / S.macro_step_H("adv1d", 0, w.n, counts, wd, w.h_factor))
+    M = 3
+    w = w.with_(steps=tuple(counts), weights=wset, macro_steps=M)
+    y0, g, info = run_gpu(torch_cuda, w, counts, wd, H, M, opts=opts)
+    o = run_oracle(w, y0, counts, wd, H, M)
+    assert info["kernel_launches"] == 2 * M * sum(k + 1 for k in counts)   # per substep: ik scale + update
+    assert_parity(g[0], o[0], what=f"spectral fft {wset} N={N}")
+
+
+def test_spectral_fft_large_grid_against_exact_solution(torch_cuda):
+    """N = 2^20 (far beyond the cluster kernel): the section 4.1 IC (1 - cos 2 pi x)/2 is one
+    Fourier mode, which the spectral derivative resolves exactly, so after M macro steps the
+    result is (1 - Re(R(H lambda)^M e^{2 pi i x}))/2 with lambda = -2 pi i -- the closed form
+    of the scheme's stability polynomial (oracle/stability.py), no O(N^2) oracle run."""
+    import math
+    N = 1 << 20
+    w = get_config("s41").with_(n=(N, 1, 1))
+    counts, ws, _ = W.scheme("GBS_8_6")
+    wd = W.to_double(ws)
+    H = 1.0 / math.ceil(1.0 / S.macro_step_H("adv1d", 0, w.n, counts, wd, w.h_factor))
+    M = 3
+    w = w.with_(steps=tuple(counts), weights="GBS_8_6", macro_steps=M)
+    y0, g, _ = run_gpu(torch_cuda, w, counts, wd, H, M)
+    amp = complex(S.R_eval(counts, wd, np.array([complex(0.0, -2.0 * math.pi * H)]))[0]) ** M
+    x = np.arange(N) / N
+    exact = 0.5 * (1.0 - (amp * np.exp(2j * math.pi * x)).real)
+    assert_parity(g[0], exact[None, :], what="spectral fft N=2^20 vs closed form")
 
 
 def test_single_sequence_and_fd4_wave(torch_cuda):
