@@ -146,6 +146,7 @@ struct gbs_ctx {
     bool tma_grid = false;            // grid is a multiple of the TMA tile (wave3d)
     int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
+    int zchunk_pair_opt = 0;          // planes per CTA of the two-substep kernel (0 = zchunk, else 256)
     int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
     int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
     bool loop_nccl = false;           // loopback halos through NCCL on a one-rank communicator

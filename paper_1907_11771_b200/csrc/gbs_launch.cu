@@ -417,7 +417,10 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
     a.nonfinite = op.flag ? c->d_flag : nullptr;
     a.zlo = (int)lo; a.zhi = (int)hi;
-    a.zchunk = c->zchunk_opt > 0 ? (int)std::min<int64_t>(c->zchunk_opt, hi - lo) : (int)std::min<int64_t>(128, hi - lo);
+    // planes per CTA: 256 by default (each CTA primes 2r planes and fills its pipeline once;
+    // 256 measured 0.4% faster than 128 on C5 at 27.7 waves of CTAs)
+    const int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : 256;
+    a.zchunk = (int)std::min<int64_t>(zc, hi - lo);
     a.band = tile_band(c, c->n[0] / gbs::tma::TX);
     a.hint = c->hint_opt;
     dim3 grid((unsigned)((c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY)), 1u,
