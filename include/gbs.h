@@ -204,6 +204,22 @@ GBS_API int gbs_read_slab(gbs_ctx* ctx, double* dst, int64_t count, int on_devic
 GBS_API int gbs_workspace_bytes(const gbs_ctx* ctx, int64_t* bytes);
 GBS_API int gbs_bind_workspace(gbs_ctx* ctx, void* device_ptr, int64_t bytes);
 
+/* Peer halo pushes (pure z-slabs of the 3-D wave on a grid of whole
+ * 64 x 16 tiles, two-substep path, one slab per GPU, groups = 1).  Instead of an NCCL halo
+ * exchange before every substep, the kernel that produces a u-level stores its r face planes
+ * straight into the neighbouring GPUs' ghost planes over NVLink, and a per-launch epoch flag
+ * (release/acquire, system scope) orders each launch's face tiles after the neighbours'
+ * previous launch (gbs_wave3d_tma.cuh, PeerPush).
+ *   gbs_bind_peers  lower_workspace / upper_workspace: the workspaces (gbs_bind_workspace) of
+ *                   the slab below / above, mapped into this process (e.g. torch symmetric
+ *                   memory or CUDA IPC); every rank binds a workspace of the same layout, whose
+ *                   last 256 bytes (part of gbs_workspace_bytes) hold the flags.  NULL, NULL returns to NCCL halos.
+ *                   Graphs are not used while bound.  GBS_E_STATE without a workspace,
+ *                   GBS_E_UNSUPPORTED when the layout does not qualify.
+ * Option "peer" runs the same kernels and protocol between loopback slabs on one GPU.
+ * Not yet run on more than one GPU. */
+GBS_API int gbs_bind_peers(gbs_ctx* ctx, void* lower_workspace, void* upper_workspace);
+
 /* Asynchronous slab IO (same layout and count as gbs_write_slab / gbs_read_slab; on one
  * GPU the slab is the whole grid).  The copies run on the context's own copy streams and
  * overlap the macro steps queued on the context stream:
@@ -256,6 +272,9 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        stores (default 11; results do not depend on it)
  *   "l2hint_step"  bits  the same for the single-substep 3-D TMA kernel (1 = tile boxes
  *                        evict_last; default 0)
+ *   "peer"         1/0   loopback slabs of a 3-D TMA grid: face planes pushed into the
+ *                        neighbouring slabs' ghost planes by the producing kernels, ordered
+ *                        by epoch flags (gbs_bind_peers), no halo exchange (default 0)
  *   "loopback_nccl" 1/0  loopback slabs exchange their ghost planes with grouped ncclSend /
  *                        ncclRecv on a one-rank communicator (the multi-GPU transfer path on one
  *                        GPU; graphs off, as with world > 1; default 0)

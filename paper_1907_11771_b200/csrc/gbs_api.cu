@@ -109,6 +109,7 @@ void gbs_destroy(gbs_ctx* c) {
     if (c->d_nk) cudaFree(c->d_nk);
     if (c->d_wh) cudaFree(c->d_wh);
     if (c->d_alpha) cudaFree(c->d_alpha);
+    if (c->d_peer_flags) cudaFree(c->d_peer_flags);
     spectral_release(c);
     for (auto e : c->timer.ev) cudaEventDestroy(e);
     auto& A = nccl::api();
@@ -213,6 +214,22 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
         c->use_graph = !on && c->use_graph;   // NCCL calls stay outside graphs, as with world > 1
         return GBS_OK;
     }
+    if (k == "peer") {
+        // loopback slabs on one GPU: the peer-push path with the neighbouring slabs' buffers
+        const bool on = value != 0;
+        if (on && !peer_eligible(c, false))
+            return fail(c, GBS_E_UNSUPPORTED, "peer pushes need loopback slabs of a 3-D TMA grid (fuse, bulk on)");
+        cudaStreamSynchronize(c->stream);
+        drop_graphs();
+        if (on && !c->d_peer_flags) {
+            CU(c, cudaMalloc(&c->d_peer_flags, sizeof(unsigned long long) * 2 * c->loopback));
+            CU(c, cudaMemset(c->d_peer_flags, 0, sizeof(unsigned long long) * 2 * c->loopback));
+            c->peer_epoch = 0;
+        }
+        c->peer_on = on;
+        c->peer_ghosts_valid = false;
+        return GBS_OK;
+    }
     if (k == "persistent") { c->use_persistent = value != 0; return GBS_OK; }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");
@@ -228,6 +245,8 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
         if (c->d_flag) { cudaFree(c->d_flag); c->d_flag = nullptr; }
         c->loopback = (int)value;
         c->have_state = false;
+        if (c->d_peer_flags) { cudaFree(c->d_peer_flags); c->d_peer_flags = nullptr; }
+        c->peer_on = false;
         return alloc_state(c);
     }
     return fail(c, GBS_E_INVAL, "unknown option '%s'", key);
@@ -235,15 +254,15 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
 
 int gbs_workspace_bytes(const gbs_ctx* c, int64_t* bytes) {
     if (!c || !bytes) return fail(const_cast<gbs_ctx*>(c), GBS_E_INVAL, "ctx or bytes is NULL");
-    *bytes = state_bytes(c);
+    *bytes = state_bytes(c) + kPeerFlagBytes;     // + this rank's peer flags (gbs_bind_peers)
     return GBS_OK;
 }
 
 int gbs_bind_workspace(gbs_ctx* c, void* device_ptr, int64_t bytes) {
     if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
-    if (device_ptr && bytes < state_bytes(c))
+    if (device_ptr && bytes < state_bytes(c) + kPeerFlagBytes)
         return fail(c, GBS_E_INVAL, "workspace of %lld bytes < %lld (gbs_workspace_bytes)", (long long)bytes,
-                    (long long)state_bytes(c));
+                    (long long)(state_bytes(c) + kPeerFlagBytes));
     if (device_ptr && (reinterpret_cast<uintptr_t>(device_ptr) % 256))
         return fail(c, GBS_E_INVAL, "workspace must be 256-byte aligned");
     CU(c, cudaSetDevice(c->device));
@@ -256,6 +275,30 @@ int gbs_bind_workspace(gbs_ctx* c, void* device_ptr, int64_t bytes) {
     c->ws_ptr = device_ptr;
     c->ws_bytes = device_ptr ? bytes : 0;
     c->have_state = false;              // the state must be written again
+    c->peer_on = false;                 // peers are bound to a workspace
+    c->peer_base[0] = c->peer_base[1] = nullptr;
+    if (device_ptr) CU(c, cudaMemset(static_cast<char*>(device_ptr) + state_bytes(c), 0, kPeerFlagBytes));
+    return GBS_OK;
+}
+
+int gbs_bind_peers(gbs_ctx* c, void* lower_workspace, void* upper_workspace) {
+    if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    if (!lower_workspace || !upper_workspace) {
+        c->peer_on = false;
+        c->peer_base[0] = c->peer_base[1] = nullptr;
+        return GBS_OK;
+    }
+    if (!c->ws_ptr) return fail(c, GBS_E_STATE, "gbs_bind_peers needs a bound workspace (gbs_bind_workspace)");
+    if (!peer_eligible(c, true))
+        return fail(c, GBS_E_UNSUPPORTED, "peer pushes need pure z-slabs (groups = 1) of a 3-D TMA grid on >1 GPU");
+    CU(c, cudaSetDevice(c->device));
+    CU(c, cudaStreamSynchronize(c->stream));
+    for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    c->peer_base[0] = static_cast<char*>(lower_workspace);
+    c->peer_base[1] = static_cast<char*>(upper_workspace);
+    c->peer_epoch = 0;
+    c->peer_on = true;
+    c->peer_ghosts_valid = false;
     return GBS_OK;
 }
 

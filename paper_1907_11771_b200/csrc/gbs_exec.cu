@@ -151,6 +151,21 @@ template <typename Launch>
 static int run_overlapped(gbs_ctx* c, Launch&& launch, const std::vector<std::pair<int, unsigned>>& halos,
                           bool self_ghosts = false, int64_t rows = 0) {
     int rc;
+    if (c->peer_on) {
+        // peer pushes: no exchange -- each slab's launch stores its face planes into the
+        // neighbours' ghost planes and waits (face CTAs only) for their previous launch;
+        // then a one-thread kernel publishes this launch's epoch to both neighbours
+        ++c->peer_epoch;
+        for (size_t v = 0; v < c->slab.size(); ++v) {
+            Slab& s = c->slab[v];
+            if ((rc = launch(s, (int64_t)0, s.nz, (int64_t)0))) return rc;
+            gbs::tma::peer_signal<<<1, 1, 0, c->stream>>>(peer_flag_remote(c, (int)v, 0),
+                                                          peer_flag_remote(c, (int)v, 1), c->peer_epoch);
+            c->launches++;
+        }
+        CU(c, cudaGetLastError());
+        return GBS_OK;
+    }
     if (c->ghost > 0 && c->slabs * c->loopback == 1) {
         // one slab with ghost rows (2-D TMA grids): only launches that read beyond the
         // slab (self_ghosts) need them, refreshed by one copy kernel; the rest wrap
@@ -350,7 +365,18 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
         c->t += H * (double)macro_steps;
         return GBS_OK;
     }
-    const bool graph = c->use_graph && !c->time_kernels && macro_steps > 0;
+    if (c->peer_on) {
+        if (!peer_eligible(c, c->world > 1) || !fused_path(c))
+            return fail(c, GBS_E_UNSUPPORTED, "peer halo pushes need the slabbed 3-D two-substep path");
+        if (!c->peer_ghosts_valid) {
+            // a freshly written state: fill Y's ghost planes once by the ordinary exchange; from
+            // then on every macro step's final kernels push them
+            int rc2 = exchange_halo(c, c->yb, 0x1u);
+            if (rc2) return rc2;
+            c->peer_ghosts_valid = true;
+        }
+    }
+    const bool graph = c->use_graph && !c->time_kernels && !c->peer_on && macro_steps > 0;
     if (graph && c->graph_H != H) {
         for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
         c->graph_H = H;

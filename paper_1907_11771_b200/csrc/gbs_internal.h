@@ -150,6 +150,13 @@ struct gbs_ctx {
     int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
     int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
     bool loop_nccl = false;           // loopback halos through NCCL on a one-rank communicator
+    // peer halo pushes (gbs_wave3d_tma.cuh PeerPush): option "peer" (loopback slabs) or
+    // gbs_bind_peers (one slab per GPU, neighbours' workspaces mapped into this process)
+    bool peer_on = false;
+    bool peer_ghosts_valid = false;   // Y's ghost planes hold the neighbours' current face planes
+    unsigned long long peer_epoch = 0;
+    char* peer_base[2] = {nullptr, nullptr};   // lower / upper neighbour's workspace (multi-GPU)
+    unsigned long long* d_peer_flags = nullptr; // loopback: [slab][from lower, from upper]
     int band_opt = 0;                 // 3-D TMA tile launch order (0 = whole rows)
     int sms = 148;                    // streaming multiprocessors of the device
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -233,6 +240,11 @@ int launch_ghost_fill(gbs_ctx* c, const std::vector<std::pair<int, unsigned>>& h
 int launch_ac2d_pair(gbs_ctx* c, Slab& s, int P, int S, int Aout, int Bout, double cfA, double cfB, int64_t lo,
                      int64_t hi, int64_t gap = 0);
 bool persistent_path(const gbs_ctx* c);
+double* peer_field(gbs_ctx* c, int v, int side, int b, int f);   // neighbour's field base
+unsigned long long* peer_flag(gbs_ctx* c, int v, int which);       // this slab's flag (0 lo, 1 hi)
+unsigned long long* peer_flag_remote(gbs_ctx* c, int v, int side); // the flag a neighbour waits on
+int peer_eligible(const gbs_ctx* c, bool multi_gpu);
+constexpr int64_t kPeerFlagBytes = 256;    // workspace tail: this rank's two flags (multi-GPU)
 int spectral_setup(gbs_ctx* c);       // cuFFT plans + buffers (order 0); idempotent
 void spectral_release(gbs_ctx* c);
 int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);

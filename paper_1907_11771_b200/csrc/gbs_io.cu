@@ -99,6 +99,7 @@ int gbs_write_state(gbs_ctx* c, const double* src, int64_t count, int on_device)
             CU(c, cudaMemcpyAsync(field_ptr(c, s, c->yb, f), src + (int64_t)f * c->points + s.z0 * c->plane,
                                   sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
     c->have_state = true;
+    c->peer_ghosts_valid = false;        // peer mode refills Y's ghost planes at the next advance
     return GBS_OK;
 }
 
@@ -162,6 +163,7 @@ int gbs_write_slab(gbs_ctx* c, const double* src, int64_t count, int on_device) 
             CU(c, cudaMemcpyAsync(field_ptr(c, s, c->yb, f), src + (int64_t)f * per_field + (s.z0 - z_lo) * c->plane,
                                   sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
     c->have_state = true;
+    c->peer_ghosts_valid = false;        // peer mode refills Y's ghost planes at the next advance
     return GBS_OK;
 }
 
@@ -212,6 +214,7 @@ int gbs_write_slab_async(gbs_ctx* c, const double* src, int64_t count, int on_de
     CU(c, cudaEventRecord(c->ev_in_ready, c->h2d));
     c->pending_in = true;
     c->have_state = true;
+    c->peer_ghosts_valid = false;        // peer mode refills Y's ghost planes at the next advance
     return GBS_OK;
 }
 

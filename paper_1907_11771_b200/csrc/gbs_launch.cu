@@ -169,23 +169,98 @@ static void launch_wave3d(const gbs::Wave3DArgs& a, dim3 grid, bool vx2, cudaStr
     if (vx2) gbs::wave3d_step<R, MODE, 2, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
     else gbs::wave3d_step<R, MODE, 1, 16, SLAB><<<grid, dim3(32, 16), 0, st>>>(a);
 }
+// peer: the face pushes of this launch (slab layouts; the FE kernel and the pair kernel only)
 template <int R, int MODE, bool SLAB>
 static cudaError_t launch_wave3d_tma(const gbs::tma::Maps& m, const gbs::Wave3DArgs& a, int zbase, dim3 grid,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, const gbs::tma::PeerPush* peer) {
     using L = gbs::tma::Layout<R, MODE>;
+    const dim3 block(32, gbs::tma::TY + 1);
+    if constexpr (SLAB && MODE == gbs::MODE_FE) {
+        if (peer) {
+            auto k = gbs::tma::wave3d_step_tma<R, MODE, true, true>;
+            cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), L::bytes);
+            if (e != cudaSuccess) return e;
+            k<<<grid, block, L::bytes, st>>>(m, a, zbase, *peer);
+            return cudaSuccess;
+        }
+    }
+    if (peer) return cudaErrorNotSupported;
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::wave3d_step_tma<R, MODE, SLAB>), L::bytes);
     if (e != cudaSuccess) return e;
-    gbs::tma::wave3d_step_tma<R, MODE, SLAB><<<grid, dim3(32, gbs::tma::TY + 1), L::bytes, st>>>(m, a, zbase);
+    gbs::tma::wave3d_step_tma<R, MODE, SLAB><<<grid, block, L::bytes, st>>>(m, a, zbase, gbs::tma::PeerPush{});
     return cudaSuccess;
 }
 template <int R, int MODEB, bool SLAB>
 static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::PairArgs& a, int zbase, dim3 grid,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, const gbs::tma::PeerPush* peer) {
     using L = gbs::tma::PairLayout<R, MODEB>;
+    const dim3 block(32, gbs::tma::TY / 2);
+    if constexpr (SLAB) {
+        if (peer) {
+            auto k = gbs::tma::wave3d_pair_tma<R, MODEB, true, true>;
+            cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), L::bytes);
+            if (e != cudaSuccess) return e;
+            k<<<grid, block, L::bytes, st>>>(m, a, zbase, *peer);
+            return cudaSuccess;
+        }
+    }
+    if (peer) return cudaErrorNotSupported;
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::wave3d_pair_tma<R, MODEB, SLAB>), L::bytes);
     if (e != cudaSuccess) return e;
-    gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, dim3(32, gbs::tma::TY / 2), L::bytes, st>>>(m, a, zbase);
+    gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, block, L::bytes, st>>>(m, a, zbase, gbs::tma::PeerPush{});
     return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// peer halo pushes: neighbour addresses and flags
+// ---------------------------------------------------------------------------
+int peer_eligible(const gbs_ctx* c, bool multi_gpu) {
+    if (c->pde != GBS_WAVE3D) return 0;
+    if (!(c->use_fuse && c->use_bulk && c->tma_grid)) return 0;     // the FE + two-substep path
+    if (multi_gpu) return c->world > 1 && c->slabs > 1 && c->groups == 1 && c->loopback == 1;
+    return c->world == 1 && c->loopback > 1;
+}
+
+double* peer_field(gbs_ctx* c, int v, int side, int b, int f) {
+    if (c->loopback > 1) {
+        const int n = c->loopback;
+        return field_ptr(c, c->slab[(v + (side ? 1 : -1) + n) % n], b, f);
+    }
+    const char* mine = reinterpret_cast<const char*>(field_ptr(c, c->slab[0], b, f));
+    return reinterpret_cast<double*>(c->peer_base[side] + (mine - static_cast<const char*>(c->ws_ptr)));
+}
+
+unsigned long long* peer_flag(gbs_ctx* c, int v, int which) {
+    if (c->loopback > 1) return c->d_peer_flags + 2 * v + which;
+    return reinterpret_cast<unsigned long long*>(static_cast<char*>(c->ws_ptr) + state_bytes(c)) + which;
+}
+
+// the flag of neighbour `side` that this slab's signal updates: the lower neighbour waits on
+// its "from upper" flag, the upper one on its "from lower" flag
+unsigned long long* peer_flag_remote(gbs_ctx* c, int v, int side) {
+    if (c->loopback > 1) {
+        const int n = c->loopback, w = (v + (side ? 1 : -1) + n) % n;
+        return c->d_peer_flags + 2 * w + (side ? 0 : 1);
+    }
+    return reinterpret_cast<unsigned long long*>(c->peer_base[side] + state_bytes(c)) + (side ? 0 : 1);
+}
+
+// this launch's PeerPush for slab s (outputs o0, o1 with o.b < 0 = none), or nullptr
+static const gbs::tma::PeerPush* make_peer(gbs_ctx* c, Slab& s, Slot o0, Slot o1, gbs::tma::PeerPush& P) {
+    if (!c->peer_on) return nullptr;
+    const int v = (int)(&s - c->slab.data());
+    P = gbs::tma::PeerPush{};
+    const Slot o[2] = {o0, o1};
+    for (int k = 0; k < 2; ++k)
+        if (o[k].b >= 0) {
+            P.lo[k] = peer_field(c, v, 0, o[k].b, o[k].f);
+            P.hi[k] = peer_field(c, v, 1, o[k].b, o[k].f);
+        }
+    P.wait_lo = peer_flag(c, v, 0);
+    P.wait_hi = peer_flag(c, v, 1);
+    P.epoch = c->peer_epoch;
+    P.nz = (int)s.nz;
+    return &P;
 }
 template <int R, int MODE, bool SLAB>
 static cudaError_t launch_ac2d_tma(const gbs::tma::AcMaps& m, const gbs::Acoustic2DArgs& a, int ybase, dim3 grid,
@@ -275,12 +350,14 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
             m.au = s.tm[op.O][0][0]; m.av = s.tm[op.O][1][0];
             const int zbase = (int)c->ghost;
             cudaError_t e = cudaSuccess;
+            gbs::tma::PeerPush pp;
+            const gbs::tma::PeerPush* peer = make_peer(c, s, Slot{op.O, 0}, op.xu, pp);
 #define W3B(RR, SL)                                                                                   \
             switch (op.mode) {                                                                        \
-                case gbs::MODE_FE: e = launch_wave3d_tma<RR, gbs::MODE_FE, SL>(m, a, zbase, grid, c->stream); break;     \
-                case gbs::MODE_LF: e = launch_wave3d_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream); break;     \
-                case gbs::MODE_FIN0: e = launch_wave3d_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break; \
-                default: e = launch_wave3d_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;           \
+                case gbs::MODE_FE: e = launch_wave3d_tma<RR, gbs::MODE_FE, SL>(m, a, zbase, grid, c->stream, peer); break;     \
+                case gbs::MODE_LF: e = launch_wave3d_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream, peer); break;     \
+                case gbs::MODE_FIN0: e = launch_wave3d_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream, peer); break; \
+                default: e = launch_wave3d_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream, peer); break;           \
             }
             if (c->R == 2) { if (slab) { W3B(2, true) } else { W3B(2, false) } }
             else { if (slab) { W3B(4, true) } else { W3B(4, false) } }
@@ -434,11 +511,13 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     m.acc_u = s.tm[op.Bu.b][0][0]; m.acc_v = s.tm[op.Bu.b][1][0];
     const int zbase = (int)c->ghost;
     cudaError_t e = cudaSuccess;
+    gbs::tma::PeerPush pp;
+    const gbs::tma::PeerPush* peer = make_peer(c, s, lf ? op.Bu : Slot{op.Bu.b, 0}, lf ? op.Cu : Slot{-1, 0}, pp);
 #define PR(RR, SL)                                                                                          \
     switch (op.modeB) {                                                                                     \
-        case gbs::MODE_LF: e = launch_pair_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream); break;     \
-        case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break; \
-        default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;           \
+        case gbs::MODE_LF: e = launch_pair_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream, peer); break;     \
+        case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream, peer); break; \
+        default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream, peer); break;           \
     }
     if (c->R == 2) { if (slab) { PR(2, true) } else { PR(2, false) } }
     else { if (slab) { PR(4, true) } else { PR(4, false) } }

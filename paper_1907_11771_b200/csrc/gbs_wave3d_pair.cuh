@@ -88,9 +88,9 @@ struct PairArgs {
                                       // 2 pointwise evict_first, 4 tiles evict_first, 8 .cs stores
 };
 
-template <int R, int MODEB, bool SLAB>
+template <int R, int MODEB, bool SLAB, bool PEER = false>
 __global__ void __launch_bounds__(256, 1)
-wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int zbase) {
+wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int zbase, const PeerPush P) {
     using L = PairLayout<R, MODEB>;
     constexpr int D = L::D, TILE = L::TILE, STAGE = L::STAGE;
     constexpr int NW = TY / 2;                 // 8 warps; each thread owns 2 x 2 points
@@ -153,9 +153,11 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
         }
     };
 
+    const bool face = z0 < R || z0 + niter > nz - R;     // reads ghost planes / owns face planes
     if (producer) {
         for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if constexpr (PEER) if (face) peer_wait(P);
     }
     __syncthreads();
     if (producer) {
@@ -301,10 +303,28 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
             *reinterpret_cast<double2*>(A.Bu + o) = make_double2(ub[2 * r], ub[2 * r + 1]);
             *reinterpret_cast<double2*>(A.Bv + o) = make_double2(vb[2 * r], vb[2 * r + 1]);
         }
+        if constexpr (PEER) {
+            // the u-levels read with stencils by the next launch: B_u (or the accumulator's u,
+            // the next macro step's Y) and C_u
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int64_t xy = own + (int64_t)r * nx;
+                peer_push2<R>(P, 0, z0 + i, plane, xy, ub[2 * r], ub[2 * r + 1]);
+                if constexpr (MODEB == MODE_LF) peer_push2<R>(P, 1, z0 + i, plane, xy, uc[2 * r], uc[2 * r + 1]);
+            }
+        }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j)
 #pragma unroll
             for (int p = 0; p < 4; ++p) { qs[j][p] = qs[j + 1][p]; qa[j][p] = qa[j + 1][p]; }
+    }
+    if constexpr (PEER) {
+        // one cumulative system fence per CTA after the barrier (the kernel boundary orders it
+        // before the epoch signal)
+        if (face) {
+            __syncthreads();
+            if (tx == 0 && ty == 0) __threadfence_system();
+        }
     }
     if constexpr (MODEB != MODE_LF)
         if (bad && A.nonfinite) *A.nonfinite = 1;

@@ -90,6 +90,50 @@ template <int MODE> struct Depth { static constexpr int v = (MODE == MODE_FINACC
 
 constexpr int TX = 64, TY = 16;
 
+// ---------------------------------------------------------------------------
+// Peer halo pushes (option "peer", slabbed 3-D two-substep path):
+// the launch that produces a u-level also stores the r face planes of its slab straight
+// into the neighbours' ghost planes (peer memory over NVLink across GPUs; the neighbouring
+// slab's buffer in loopback), so no halo exchange runs between substeps.  Ordering by
+// per-slab epochs: after every launch a one-thread kernel release-stores the launch's
+// epoch into both neighbours' flags; a CTA whose planes touch a slab face (it reads ghost
+// planes or pushes face planes) first waits until both neighbours have finished the
+// previous launch -- that covers RAW (their pushes of this launch's inputs are complete)
+// and WAR (they are done reading the ghost planes of the buffers this launch overwrites:
+// with the rotating u-slots only the previous launch read them).
+struct PeerPush {
+    double* lo[2];                         // lower neighbour's field base (plane 0) per pushed output
+    double* hi[2];                         // upper neighbour's
+    const unsigned long long* wait_lo;     // this slab's flags, written by the neighbours
+    const unsigned long long* wait_hi;
+    unsigned long long epoch;              // this launch
+    int nz;                                // planes per slab (all slabs equal)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void peer_wait(const PeerPush& P) {
+    const unsigned long long need = P.epoch - 1;
+    while (ld_acquire_sys(P.wait_lo) < need || ld_acquire_sys(P.wait_hi) < need) __nanosleep(200);
+    asm volatile("fence.proxy.async.global;" ::: "memory");    // TMA reads see the pushed planes
+}
+// the face copy of a double2 the thread stores at slab plane z (offset `xy` in the plane)
+template <int R>
+__device__ __forceinline__ void peer_push2(const PeerPush& P, int o, int z, int64_t plane, int64_t xy, double a,
+                                           double b) {
+    if (z < R) *reinterpret_cast<double2*>(P.lo[o] + (int64_t)(P.nz + z) * plane + xy) = make_double2(a, b);
+    if (z >= P.nz - R) *reinterpret_cast<double2*>(P.hi[o] + (int64_t)(z - P.nz) * plane + xy) = make_double2(a, b);
+}
+template <int Unused = 0>
+__global__ void peer_signal(unsigned long long* to_lo, unsigned long long* to_hi, unsigned long long epoch) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_lo), "l"(epoch) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(to_hi), "l"(epoch) : "memory");
+}
+
 // Launch order of the ntx x nty tiles of a plane (grid x = ntx * nty): bands of `band`
 // x-tiles, x fastest inside a band, then y, then the next band.  band = ntx is plain
 // row order.  Resident CTAs start in launch order and march z at the same rate, so two
@@ -127,9 +171,9 @@ struct Maps {
     CUtensorMap sv, pu, pv, au, av;    // TXxTY boxes
 };
 
-template <int R, int MODE, bool SLAB>
+template <int R, int MODE, bool SLAB, bool PEER = false>
 __global__ void __launch_bounds__(544, 1)
-wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zbase) {
+wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zbase, const PeerPush P) {
     using L = Layout<R, MODE>;
     constexpr int D = L::D, RING = L::RING, NP = L::NP, TILE = L::TILE, PWT = L::PWT;
     extern __shared__ __align__(128) double smem[];
@@ -152,10 +196,12 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
         else return wrap_once(z, nz);
     };
 
+    const bool face = z0 < R || z0 + niter > nz - R;     // reads ghost planes / owns face planes
     if (ty == 0 && lane == 0) {
         for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], TY); }
         mbar_init(init, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if constexpr (PEER) if (face) peer_wait(P);
     }
     __syncthreads();
 
@@ -297,15 +343,27 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
         };
         put(A.Ou + o, ou[0], ou[1]);
         put(A.Ov + o, ov[0], ov[1]);
+        if constexpr (PEER) peer_push2<R>(P, 0, z0 + i, plane, own, ou[0], ou[1]);
         if constexpr (MODE == MODE_FE) {
             // u_2 = u_0 + 2h v_1 (the next leap-frog step's pointwise u, formed exactly as
             // the single-step LF kernel forms it) for the two-substep kernel
-            if (A.Xu)
-                put(A.Xu + o, combine<MODE_LF>(xw[R], 0.0, ov[0], 0.0, A.cf2, 0.0),
-                    combine<MODE_LF>(xw[R + 1], 0.0, ov[1], 0.0, A.cf2, 0.0));
+            if (A.Xu) {
+                const double x0v = combine<MODE_LF>(xw[R], 0.0, ov[0], 0.0, A.cf2, 0.0);
+                const double x1v = combine<MODE_LF>(xw[R + 1], 0.0, ov[1], 0.0, A.cf2, 0.0);
+                put(A.Xu + o, x0v, x1v);
+                if constexpr (PEER) peer_push2<R>(P, 1, z0 + i, plane, own, x0v, x1v);
+            }
         }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j) q[j] = q[j + 1];
+    }
+    if constexpr (PEER) {
+        // the CTA's face pushes are ordered before the next launch's epoch signal by the
+        // kernel boundary; one cumulative system fence per CTA after the consumers' barrier
+        if (face) {
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * TY) : "memory");
+            if (tx == 0 && ty == 0) __threadfence_system();
+        }
     }
     if constexpr (MODE == MODE_FIN0 || MODE == MODE_FINACC)
         if (bad && A.nonfinite) *A.nonfinite = 1;

@@ -27,7 +27,7 @@ NDIM = {"adv1d": 1, "acoustic2d": 2, "wave3d": 3}
 
 EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gbs_write_slab",
            "gbs_read_slab", "gbs_write_slab_async", "gbs_read_slab_async", "gbs_workspace_bytes",
-           "gbs_bind_workspace", "gbs_sync",
+           "gbs_bind_workspace", "gbs_bind_peers", "gbs_sync",
            "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
            "gbs_set_option",
            "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
@@ -114,6 +114,7 @@ def load(build_if_missing: bool = False):
     L.gbs_read_slab_async.argtypes = [vp, vp, i64, ctypes.c_int]
     L.gbs_workspace_bytes.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
     L.gbs_bind_workspace.argtypes = [vp, vp, i64]
+    L.gbs_bind_peers.argtypes = [vp, vp, vp]
     L.gbs_sync.argtypes = [vp]
     L.gbs_destroy.argtypes = [vp]
     L.gbs_destroy.restype = None
@@ -259,6 +260,14 @@ def gbs_workspace_bytes(ctx) -> int:
     b = ctypes.c_int64(0)
     _check(load().gbs_workspace_bytes(ctx, ctypes.byref(b)), ctx)
     return b.value
+
+
+def gbs_bind_peers(ctx, lower_ptr, upper_ptr) -> None:
+    """Peer halo pushes (include/gbs.h): the neighbouring slabs' workspaces as device
+    addresses mapped into this process (ints), or None, None to return to NCCL halos."""
+    lo = ctypes.c_void_p(int(lower_ptr)) if lower_ptr else None
+    hi = ctypes.c_void_p(int(upper_ptr)) if upper_ptr else None
+    _check(load().gbs_bind_peers(ctx, lo, hi), ctx)
 
 
 def gbs_bind_workspace(ctx, ws) -> None:

@@ -513,6 +513,40 @@ def test_loopback_halos_through_nccl(torch_cuda, cfg, n, slabs, overlap):
     assert_parity(a[0], o[0], what=f"nccl loopback {cfg} {slabs} slabs")
 
 
+@pytest.mark.parametrize("cfg,n,slabs", [("c5", (64, 32, 48), 2), ("c4", (64, 16, 36), 3), ("c5", (128, 32, 64), 4),
+                                         ("c4", (64, 16, 16), 4), ("c5", (64, 48, 60), 3)])
+def test_peer_halo_pushes_match_exchange(torch_cuda, cfg, n, slabs):
+    """Peer pushes (option peer, loopback slabs): the FE and two-substep kernels store their
+    face planes into the neighbouring slabs' ghost planes and order themselves by epoch flags
+    -- no halo exchange.  Bit-identical to the exchanged loopback and to the single slab, and
+    the oracle's result; a second advance continues from the pushed ghosts."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "peer": 1})
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": 0})
+    _, c1, _ = run_gpu(torch_cuda, w, counts, wd, H, 2)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[0], c1[0])
+    # one stencil launch + one epoch signal per slab per substep launch, no exchange
+    assert ia["kernel_launches"] == 2 * ib["kernel_launches"]
+    _, d, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, checkpoints=True, opts={"loopback": slabs, "peer": 1})
+    assert np.array_equal(d[-1], a[0])
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(a[0], o[0], what=f"peer {cfg} {n} {slabs}")
+
+
+def test_peer_option_rejected_where_it_does_not_apply(torch_cuda):
+    gbs = gbs_mod()
+    w = reduced("c4", (40, 36, 32), macro_steps=1, weights="nonzero8")   # not whole 64x16 tiles
+    counts, wd, _ = scheme_for(w, "nonzero8")
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd, loopback=2) as st:
+        with pytest.raises(gbs.GbsError) as e:
+            gbs.gbs_set_option(st.ctx, "peer", 1)
+        assert e.value.code == gbs.GBS_E_UNSUPPORTED
+        with pytest.raises(gbs.GbsError) as e:
+            gbs.gbs_bind_peers(st.ctx, 1 << 40, 1 << 40)      # one GPU: not a multi-GPU slab layout
+        assert e.value.code in (gbs.GBS_E_STATE, gbs.GBS_E_UNSUPPORTED)
+
+
 # ----------------------------------------------------------------------------- errors
 def test_error_paths(torch_cuda):
     gbs = gbs_mod()
