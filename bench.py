@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--groups", type=int, default=0, help="sequence groups (0 = planner)")
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
                     help="library option (gbs_set_option) for this run, e.g. pdl=0")
+    ap.add_argument("--peers", action="store_true",
+                    help="N > 1: halo planes pushed by the stencil kernels into the neighbours' "
+                         "ghost planes through torch symmetric memory (gbs_bind_peers) instead of NCCL")
     ap.add_argument("--repeats", type=int, default=3,
                     help="extra K-step timed regions after the metric's (median / best reported "
                          "under 'repeats'; 'value' stays the first region)")
@@ -267,7 +270,7 @@ def run_ours(a):
         # the state buffers live in a torch tensor (gbs_bind_workspace): PyTorch owns device memory
         opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
         st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream,
-                         torch_memory=True, **opts)
+                         torch_memory=True, peers=a.peers and world > 1, **opts)
         y0_dev = torch.from_numpy(y0).to("cuda", non_blocking=False)
         st.write_slab(y0_dev)
         gbs.gbs_sync(st.ctx)
@@ -442,6 +445,8 @@ def run_ours(a):
                                   "%.0f MiB < 2 x L2" % (6 * y0.nbytes / 2 ** 20) if flush else
                                   "inputs larger than L2 (each state buffer %.2f GiB)" % (y0.nbytes / 2 ** 30)),
                            "plan": {"groups": info["groups"], "slabs": info["slabs"]},
+                           "halo": ("peer pushes (symmetric memory)" if a.peers and world > 1 else
+                                    "NCCL send/recv overlapped with the interior" if info["slabs"] > 1 else "none"),
                            "hbm_roofline_fraction_of_step": round(
                                value * 24 * F / (peak * 1e9 * world), 4)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -315,21 +315,53 @@ def gbs_last_error(ctx=None) -> str:
     return load().gbs_last_error(ctx).decode()
 
 
+def peer_neighbours(pde, n, stencil_order, n_k, world: int, rank: int, groups: int = 0):
+    """Ranks holding slab my_slab - 1 and my_slab + 1 (periodic) of this rank's sequence group,
+    from the host-only plans of every rank."""
+    plans = [gbs_plan(pde, n, stencil_order, n_k, world, r, groups) for r in range(world)]
+    me = plans[rank]
+    where = {(p["my_group"], p["my_slab"]): r for r, p in enumerate(plans)}
+    return (where[(me["my_group"], (me["my_slab"] - 1) % me["slabs"])],
+            where[(me["my_group"], (me["my_slab"] + 1) % me["slabs"])])
+
+
 class Stepper:
     """RAII convenience around one context (still only marshalling)."""
 
-    def __init__(self, pde, n, stencil_order, n_k, w_k, dist=None, stream=None, torch_memory=False, **opts):
+    def __init__(self, pde, n, stencil_order, n_k, w_k, dist=None, stream=None, torch_memory=False,
+                 peers=False, **opts):
         self.pde = pde
         self.ctx = gbs_create(pde, n, stencil_order, n_k, w_k, dist, stream)
         for k, v in opts.items():
             gbs_set_option(self.ctx, k, v)
         self.workspace = None
-        if torch_memory:
+        self.symm = None
+        if torch_memory or peers:
             # the state buffers live in a torch tensor (PyTorch's allocator owns the memory)
             import torch
-            nbytes = gbs_workspace_bytes(self.ctx)
-            self.workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
-            gbs_bind_workspace(self.ctx, self.workspace)
+            nbytes = max(gbs_workspace_bytes(self.ctx), 1)
+            if peers and dist and dist.get("world", 1) > 1:
+                self.workspace = self._peer_workspace(pde, n, stencil_order, n_k, dist, nbytes)
+            else:
+                self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                gbs_bind_workspace(self.ctx, self.workspace)
+
+    def _peer_workspace(self, pde, n, stencil_order, n_k, dist, nbytes):
+        """Peer halo pushes across GPUs (include/gbs.h gbs_bind_peers): the workspace is torch
+        symmetric memory, every rank's mapped into every other; the neighbours are the ranks
+        holding slab my_slab -/+ 1 of the same sequence group (collective over all ranks)."""
+        import torch
+        import torch.distributed as tdist
+        import torch.distributed._symmetric_memory as symm
+        lo, hi = peer_neighbours(pde, n, stencil_order, n_k, dist["world"], dist["rank"], dist.get("groups", 0))
+        ws = symm.empty(nbytes, dtype=torch.uint8, device="cuda")
+        gbs_bind_workspace(self.ctx, ws)
+        self.symm = symm.rendezvous(ws, tdist.group.WORLD)
+        torch.cuda.synchronize()
+        tdist.barrier()                          # every rank's flags are zeroed before any push
+        ptrs = self.symm.buffer_ptrs
+        gbs_bind_peers(self.ctx, ptrs[lo], ptrs[hi])
+        return ws
 
     def write(self, y):
         gbs_write_state(self.ctx, y)

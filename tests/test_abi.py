@@ -99,3 +99,19 @@ def test_argument_validation_precedes_device(lib):
         with pytest.raises(gbs.GbsError) as e:
             gbs.gbs_create(*args, stream=0)
         assert e.value.code == code, (args, e.value)
+
+
+def test_peer_neighbours_are_the_adjacent_slabs_of_the_group():
+    """Host logic of gbs_bind_peers' callers: the ranks holding the slabs below / above."""
+    from paper_1907_11771_b200 import gbs
+    steps = list(range(2, 17, 2))
+    for world, groups in ((2, 1), (4, 1), (8, 1), (8, 2), (8, 4)):
+        plans = [gbs.gbs_plan("wave3d", (1024, 1024, 1024), 8, steps, world, r, groups) for r in range(world)]
+        for r in range(world):
+            lo, hi = gbs.peer_neighbours("wave3d", (1024, 1024, 1024), 8, steps, world, r, groups)
+            me, pl, ph = plans[r], plans[lo], plans[hi]
+            assert pl["my_group"] == me["my_group"] == ph["my_group"]
+            s = me["slabs"]
+            assert pl["my_slab"] == (me["my_slab"] - 1) % s and ph["my_slab"] == (me["my_slab"] + 1) % s
+            # the lower neighbour's slab ends where this one starts (periodically)
+            assert (pl["slab_z0"] + pl["slab_nz"]) % 1024 == me["slab_z0"]
