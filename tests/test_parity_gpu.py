@@ -745,6 +745,9 @@ def _random_cases(seed=20261020, count=14, include_1d=False):
             opts["fuse2d"] = int(rng.integers(0, 2))
         if lb > 1 and rng.integers(0, 4) == 0:
             opts["loopback_nccl"] = 1
+        if (cfg in ("c4", "c5") and lb > 1 and n[0] % 64 == 0 and n[1] % 16 == 0 and opts["fuse"]
+                and rng.integers(0, 2) == 0):
+            opts["peer"] = 1
         cases.append((cfg, n, opts))
     return cases
 
