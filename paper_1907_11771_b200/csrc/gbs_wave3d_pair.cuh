@@ -92,7 +92,7 @@ template <int R, int MODEB, bool SLAB, bool PEER = false>
 __global__ void __launch_bounds__(256, 1)
 wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int zbase, const PeerPush P) {
     using L = PairLayout<R, MODEB>;
-    constexpr int D = L::D, TILE = L::TILE, STAGE = L::STAGE;
+    constexpr int D = L::D, STAGE = L::STAGE;
     constexpr int NW = TY / 2;                 // 8 warps; each thread owns 2 x 2 points
     constexpr int Q = 2 * R + 1;
     extern __shared__ __align__(128) double smem[];
