@@ -156,7 +156,11 @@ def workload_and_scheme(name, weights=None):
     w = get_config(name)
     if weights:
         w = w.with_(weights=weights)
-    counts, ws, _ = scheme.weight_set(w.weights, w.steps)
+    try:
+        counts, ws, _ = scheme.weight_set(w.weights, w.steps)
+    except ValueError:                          # a paper scheme (e.g. GBS_8_8) brings its own counts
+        counts, ws, _ = scheme.weight_set(w.weights)
+    w = w.with_(steps=tuple(counts))
     wd = scheme.to_fp64(ws)
     H = scheme.macro_step(w.pde, w.order, w.n, counts, wd, w.h_factor)
     return w, counts, wd, H
