@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--peers", action="store_true",
                     help="N > 1: halo planes pushed by the stencil kernels into the neighbours' "
                          "ghost planes through torch symmetric memory (gbs_bind_peers) instead of NCCL")
-    ap.add_argument("--repeats", type=int, default=3,
+    ap.add_argument("--repeats", type=int, default=5,
                     help="extra K-step timed regions after the metric's (median / best reported "
                          "under 'repeats'; 'value' stays the first region)")
     ap.add_argument("--weights", default=None,
@@ -120,7 +120,9 @@ class ClockSampler:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
                 rs = get_reasons(h)
-                self.rows.append([str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in self.BITS])
+                mem = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)
+                self.rows.append([str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in self.BITS]
+                                 + [str(mem)])
             except Exception:
                 return
             self.stop_flag.wait(0.002)
@@ -146,7 +148,9 @@ class ClockSampler:
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        mem = [float(r[6]) for r in self.rows if len(r) > 6 and r[6].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "mem_mhz": statistics.median(mem) if mem else None,
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 

@@ -263,7 +263,7 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        a gbs_advance in one thread-block-cluster launch (default 1)
  *   "zchunk"       k     planes per CTA along the slowest axis (0 = automatic)
  *   "zchunk_pair"  k     the same for the two-substep 3-D kernel only (0 = "zchunk" if set,
- *                        else 256)
+ *                        else 256 when that leaves >= 8 waves of CTAs, otherwise 128)
  *   "band"         b     3-D TMA kernels: launch the x-y tiles in bands of b x-tiles (x fastest
  *                        inside a band); 0 or a b that does not divide the x-tile count =
  *                        whole rows (default 0; results do not depend on it)

@@ -494,9 +494,12 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
     a.nonfinite = op.flag ? c->d_flag : nullptr;
     a.zlo = (int)lo; a.zhi = (int)hi;
-    // planes per CTA: 256 by default (each CTA primes 2r planes and fills its pipeline once;
-    // 256 measured 0.4% faster than 128 on C5 at 27.7 waves of CTAs)
-    const int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : 256;
+    // planes per CTA: each CTA primes 2r planes and fills its pipeline once, so longer chunks
+    // save a little (256 vs 128: +0.4% on C5 at 27.7 waves of CTAs) -- but only while the grid
+    // keeps >= 8 waves (C4 at 256 planes: 3.5 waves, 5% slower than 128)
+    const int64_t tiles = (c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY);
+    const int zauto = tiles * ((hi - lo + 255) / 256) >= 8LL * c->sms ? 256 : 128;
+    const int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : zauto;
     a.zchunk = (int)std::min<int64_t>(zc, hi - lo);
     a.band = tile_band(c, c->n[0] / gbs::tma::TX);
     a.hint = c->hint_opt;
