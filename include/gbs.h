@@ -79,6 +79,11 @@ typedef struct gbs_grid {
 } gbs_grid;
 
 /* Multi-GPU description (one process per GPU).  Pass NULL for a single GPU. */
+#define GBS_TRANSPORT_NCCL   0   /* one process per GPU, NCCL communicators (production) */
+#define GBS_TRANSPORT_LOCAL  1   /* every rank is a context of this process on ONE device,
+                                    driven by its own host thread; collectives are device
+                                    copies ordered by events and host barriers (tests and
+                                    emulation of N ranks on one GPU; gbs_local_hub_create) */
 typedef struct gbs_dist {
     int32_t rank;            /* this process's rank in [0, world) */
     int32_t world;           /* number of GPUs / processes */
@@ -87,7 +92,22 @@ typedef struct gbs_dist {
                                 world / g ranks share each group as z-slabs (y in 2-D) */
     uint8_t nccl_id[128];    /* ncclUniqueId made by gbs_nccl_unique_id on rank 0 and
                                 broadcast by the caller (e.g. torch.distributed) */
+    int32_t transport;       /* GBS_TRANSPORT_NCCL (0) or GBS_TRANSPORT_LOCAL */
+    int32_t pad;
+    void*   hub;             /* GBS_TRANSPORT_LOCAL: the hub shared by the world's contexts */
 } gbs_dist;
+
+/* In-process transport for `world` contexts on one device (GBS_TRANSPORT_LOCAL): create the
+ * hub once, pass it in every rank's gbs_dist, call gbs_create / gbs_advance / gbs_read_state
+ * of the ranks from `world` concurrent host threads (collectives block until every member of
+ * the communicator arrives; a member missing for 300 s fails them with GBS_E_NCCL), destroy
+ * the hub after every context.  The macro step runs the same plan, halo schedule, group
+ * combine and gather as over NCCL: halo planes by device-to-device copies matched in NCCL's
+ * posting order, the combine as one kernel per rank that sums its share of the elements over
+ * the group members in member order and stores the sum into every member (deterministic).
+ * No kernel waits on another rank's kernel.  Not a performance path: the ranks share one GPU. */
+GBS_API int gbs_local_hub_create(int world, int device, void** hub);
+GBS_API void gbs_local_hub_destroy(void* hub);
 
 /* Plan and accounting, filled by gbs_query. */
 typedef struct gbs_info {

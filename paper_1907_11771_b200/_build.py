@@ -29,7 +29,8 @@ def sources():
 
 def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + \
-        [os.path.join(ROOT, "include", "gbs.h"), __file__]
+        sorted(glob.glob(os.path.join(CSRC, "*.h"))) + \
+        sorted(glob.glob(os.path.join(ROOT, "include", "*.h"))) + [__file__]
 
 
 def up_to_date() -> bool:
@@ -43,18 +44,35 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-o", tmp, *sources(), "-ldl"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     log = os.path.join(LIBDIR, "build.log")
+    # one nvcc per translation unit, in parallel, then one link
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *NVCC_FLAGS, *inc, "-c", "-o", obj, src]
+        jobs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    out, failed = [], False
+    for cmd, obj, pr in jobs:
+        text = pr.communicate()[0]
+        out.append(" ".join(cmd) + "\n" + text)
+        failed |= pr.returncode != 0
+    tmp = LIB + f".tmp{os.getpid()}"
+    if not failed:
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
+               *[o for _, o, _ in jobs], "-ldl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        out.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        failed = r.returncode != 0
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
+        f.write("\n".join(out))
+    if failed:
+        sys.stderr.write("\n".join(out))
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write("\n".join(out))
     os.replace(tmp, LIB)
     return LIB
 

@@ -112,12 +112,7 @@ void gbs_destroy(gbs_ctx* c) {
     if (c->d_peer_flags) cudaFree(c->d_peer_flags);
     spectral_release(c);
     for (auto e : c->timer.ev) cudaEventDestroy(e);
-    auto& A = nccl::api();
-    if (A.ok) {
-        if (c->comm_group) A.CommDestroy(c->comm_group);
-        if (c->comm_slab) A.CommDestroy(c->comm_slab);
-        if (c->comm_world) A.CommDestroy(c->comm_world);
-    }
+    comm_release(c);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -156,21 +151,8 @@ int gbs_create(const gbs_grid* g, int stencil_order, int m, const int32_t* n_k, 
     if ((rc0 = make_plan(c, dist ? dist->rank : 0, dist ? dist->world : 1, dist ? dist->groups : 0)))
         return bail(rc0);
     if (c->world > 1) {
-        auto& A = nccl::api();
-        if (!A.ok) return bail(fail(c, GBS_E_NCCL, "libnccl.so.2 not found"));
-        nccl::uid_t id;
-        memcpy(&id, dist->nccl_id, 128);
-        int r = A.CommInitRank(&c->comm_world, c->world, id, c->rank);
-        if (r) return bail(fail(c, GBS_E_NCCL, "ncclCommInitRank: %s", A.GetErrorString(r)));
-        if (c->slabs > 1) {
-            r = A.CommSplit(c->comm_world, c->my_group, c->my_slab, &c->comm_slab, nullptr);
-            if (r) return bail(fail(c, GBS_E_NCCL, "ncclCommSplit(slab): %s", A.GetErrorString(r)));
-        }
-        if (c->groups > 1) {
-            r = A.CommSplit(c->comm_world, c->my_slab, c->my_group, &c->comm_group, nullptr);
-            if (r) return bail(fail(c, GBS_E_NCCL, "ncclCommSplit(group): %s", A.GetErrorString(r)));
-        }
-        c->use_graph = false;   // NCCL calls stay outside graphs
+        if ((rc0 = comm_init(c, dist))) return bail(rc0);
+        c->use_graph = false;   // collectives stay outside graphs
     }
     int rc = build_ctx(c);
     if (rc) return bail(rc);
@@ -201,12 +183,8 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
         if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback_nccl needs a single-GPU context");
         const bool on = value != 0;
         if (on && !c->comm_slab) {
-            auto& A = nccl::api();
-            if (!A.ok) return fail(c, GBS_E_NCCL, "libnccl.so.2 not found");
-            nccl::uid_t id;
-            int r = A.GetUniqueId(&id);
-            if (!r) r = A.CommInitRank(&c->comm_slab, 1, id, 0);
-            if (r) return fail(c, GBS_E_NCCL, "one-rank communicator: %s", A.GetErrorString(r));
+            int rc = comm_nccl_self(c, &c->comm_slab);
+            if (rc) return rc;
         }
         cudaStreamSynchronize(c->stream);
         drop_graphs();
@@ -289,6 +267,9 @@ int gbs_bind_peers(gbs_ctx* c, void* lower_workspace, void* upper_workspace) {
         return GBS_OK;
     }
     if (!c->ws_ptr) return fail(c, GBS_E_STATE, "gbs_bind_peers needs a bound workspace (gbs_bind_workspace)");
+    if (c->local_transport)
+        return fail(c, GBS_E_UNSUPPORTED, "peer pushes between contexts of one process (local transport): their "
+                                          "kernels would wait on one another's launches on one GPU");
     if (!peer_eligible(c, true))
         return fail(c, GBS_E_UNSUPPORTED, "peer pushes need pure z-slabs (groups = 1) of a 3-D TMA grid on >1 GPU");
     CU(c, cudaSetDevice(c->device));

@@ -39,23 +39,23 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st =
         // into the ghost planes, on the comm stream under overlap -- exercised on one GPU).
         // Every operation has peer 0, and NCCL pairs sends and receives to one peer in
         // posting order, so the receives are posted in the order of their matching sends.
-        auto& A = nccl::api();
-        NC(c, A.GroupStart());
+        Comm* K = c->comm_slab;
+        int rc;
+        if ((rc = K->group_start(c))) return rc;
         for (int v = 0; v < nloc; ++v)
             for (int f : fields) {
-                const double* base = field_ptr(c, c->slab[v], b, f);
-                NC(c, A.Send(base + (c->slab[v].nz - G) * P, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));  // up
-                NC(c, A.Send(base, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));                           // down
+                double* base = field_ptr(c, c->slab[v], b, f);
+                if ((rc = K->send(c, base + (c->slab[v].nz - G) * P, cnt, 0, st))) return rc;   // up
+                if ((rc = K->send(c, base, cnt, 0, st))) return rc;                             // down
             }
         for (int v = 0; v < nloc; ++v)
             for (int f : fields) {
                 Slab& up = c->slab[(v + 1) % nloc];
                 Slab& dn = c->slab[(v - 1 + nloc) % nloc];
-                NC(c, A.Recv(field_ptr(c, up, b, f) - G * P, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));
-                NC(c, A.Recv(field_ptr(c, dn, b, f) + dn.nz * P, cnt, nccl::ncclFloat64, 0, c->comm_slab, st));
+                if ((rc = K->recv(c, field_ptr(c, up, b, f) - G * P, cnt, 0, st))) return rc;
+                if ((rc = K->recv(c, field_ptr(c, dn, b, f) + dn.nz * P, cnt, 0, st))) return rc;
             }
-        NC(c, A.GroupEnd());
-        return GBS_OK;
+        return K->group_end(c, st);
     }
     if (c->slabs == 1) {
         // all slabs local: device-to-device copies
@@ -76,20 +76,20 @@ static int exchange_halo(gbs_ctx* c, int b, unsigned mask = 0, cudaStream_t st =
         return GBS_OK;
     }
     if (nloc != 1) return fail(c, GBS_E_UNSUPPORTED, "loopback slabs with multi-GPU slabs");
-    auto& A = nccl::api();
     Slab& me = c->slab[0];
     unsigned fm = 0;
     for (int f : fields) fm |= 1u << f;
     const std::vector<gbs_halo_op> ops = halo_schedule(c->slabs, c->my_slab, me.nz, (int)G, fm);
-    NC(c, A.GroupStart());
+    Comm* K = c->comm_slab;
+    int rc;
+    if ((rc = K->group_start(c))) return rc;
     for (const auto& op : ops) {
         double* p = field_ptr(c, me, b, op.field) + op.plane0 * P;
         const size_t n = (size_t)(op.planes * P);
-        if (op.kind == 0) NC(c, A.Send(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, st));
-        else NC(c, A.Recv(p, n, nccl::ncclFloat64, op.peer, c->comm_slab, st));
+        rc = op.kind == 0 ? K->send(c, p, n, op.peer, st) : K->recv(c, p, n, op.peer, st);
+        if (rc) return rc;
     }
-    NC(c, A.GroupEnd());
-    return GBS_OK;
+    return K->group_end(c, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -334,15 +334,15 @@ static int enqueue_macro(gbs_ctx* c, double H) {
         first = false;
     }
     if (c->groups > 1) {
-        auto& A = nccl::api();
+        // Y <- sum over the sequence groups of their w-scaled partial sums
         Slab& s = c->slab[0];
-        NC(c, A.GroupStart());
+        double* p[3];
+        size_t n[3];
         for (int f = 0; f < c->F; ++f) {
-            double* p = field_ptr(c, s, ACC, f);
-            NC(c, A.AllReduce(p, p, (size_t)(s.nz * c->plane), nccl::ncclFloat64, nccl::ncclSum,
-                              c->comm_group, c->stream));
+            p[f] = field_ptr(c, s, ACC, f);
+            n[f] = (size_t)(s.nz * c->plane);
         }
-        NC(c, A.GroupEnd());
+        if ((rc = c->comm_group->allreduce_sum(c, p, n, c->F, c->stream))) return rc;
     }
     c->yb = ACC;
     c->launches_per_macro = c->launches - l0;

@@ -70,6 +70,30 @@ Api& api();                        // gbs_api.cu
 }  // namespace cufft
 
 // ---------------------------------------------------------------------------
+// Collectives of the macro step (gbs_comm.cu): NCCL (one process per GPU) or the
+// in-process local transport (every rank a context of this process on one device).
+// ---------------------------------------------------------------------------
+struct gbs_ctx;
+struct Comm {
+    int rank = 0, size = 1;
+    virtual ~Comm() {}
+    virtual bool is_nccl() const = 0;
+    // grouped point-to-point (the halo planes): posted between group_start and group_end
+    virtual int group_start(gbs_ctx* c) = 0;
+    virtual int send(gbs_ctx* c, const double* p, size_t n, int peer, cudaStream_t st) = 0;
+    virtual int recv(gbs_ctx* c, double* p, size_t n, int peer, cudaStream_t st) = 0;
+    virtual int group_end(gbs_ctx* c, cudaStream_t st) = 0;
+    // in place: p[i][0..n[i]) <- sum over the members (k buffers, one collective group)
+    virtual int allreduce_sum(gbs_ctx* c, double* const* p, const size_t* n, int k, cudaStream_t st) = 0;
+    // dst[j*n .. (j+1)*n) <- member j's src
+    virtual int allgather(gbs_ctx* c, const double* src, double* dst, size_t n, cudaStream_t st) = 0;
+    virtual int split(gbs_ctx* c, int color, int key, Comm** out) = 0;
+};
+int comm_init(gbs_ctx* c, const gbs_dist* d);   // world, slab and group communicators
+int comm_nccl_self(gbs_ctx* c, Comm** out);      // one-rank NCCL communicator (loopback_nccl)
+void comm_release(gbs_ctx* c);
+
+// ---------------------------------------------------------------------------
 struct Slab {
     int64_t z0 = 0, nz = 0;           // interior planes [z0, z0 + nz) of the slowest axis
     double* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // Y, ACC, L0..L3 (+ ghosts)
@@ -105,7 +129,10 @@ struct gbs_ctx {
     // distribution
     int rank = 0, world = 1, device = 0, groups = 1, slabs = 1, my_group = 0, my_slab = 0;
     int loopback = 1;                 // local slabs on this GPU
-    nccl::comm_t comm_world = nullptr, comm_slab = nullptr, comm_group = nullptr;
+    Comm* comm_world = nullptr;       // all ranks
+    Comm* comm_slab = nullptr;        // the slabs of this rank's sequence group (halo exchange, gather)
+    Comm* comm_group = nullptr;       // the groups holding this rank's slab (combine)
+    bool local_transport = false;     // ranks are contexts of this process (gbs_local_hub_create)
     // memory
     std::vector<Slab> slab;
     int64_t ghost = 0;                // ghost planes per side (R when slabbed)

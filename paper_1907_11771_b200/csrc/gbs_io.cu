@@ -129,13 +129,12 @@ int gbs_read_state(gbs_ctx* c, double* dst, int64_t count, int on_device) {
                 CU(c, cudaMemcpyAsync(dst + (int64_t)f * c->points + s.z0 * c->plane, field_ptr(c, s, c->yb, f),
                                       sizeof(double) * (size_t)(s.nz * c->plane), kind, c->stream));
     } else {
-        auto& A = nccl::api();
         Slab& s = c->slab[0];
         const size_t slab_cnt = (size_t)(s.nz * c->plane);
         if (!c->d_gather) CU(c, cudaMalloc(&c->d_gather, sizeof(double) * (size_t)c->points));
         for (int f = 0; f < c->F; ++f) {
-            NC(c, A.AllGather(field_ptr(c, s, c->yb, f), c->d_gather, slab_cnt, nccl::ncclFloat64,
-                              c->comm_slab, c->stream));
+            int rc = c->comm_slab->allgather(c, field_ptr(c, s, c->yb, f), c->d_gather, slab_cnt, c->stream);
+            if (rc) return rc;
             CU(c, cudaMemcpyAsync(dst + (int64_t)f * c->points, c->d_gather, sizeof(double) * (size_t)c->points,
                                   kind, c->stream));
         }

@@ -7,45 +7,79 @@
 // ---------------------------------------------------------------------------
 // planning
 // ---------------------------------------------------------------------------
-// Partition sequence indices into g groups with balanced sum(n_k + 1): longest
-// processing time first, then pairwise moves/swaps while the maximum drops.
+// Partition sequence indices into g groups minimising the largest group load
+// sum(n_k + 1) (§3.6: sequences folded onto cores so that
+// every core does the same number of RHS evaluations; exact
+// search, m <= 32).  Exact branch and bound: sequences in descending load,
+// each placed into a group whose load stays below the best maximum found so
+// far, never into two groups of equal load (symmetry), stopped at the lower
+// bound max(ceil(total / g), largest load).  The initial bound is the LPT
+// (longest processing time first) partition, which is also the answer if the
+// search exceeds its node budget (never for the step sets of the configs and
+// the paper's schemes, which finish in well under a millisecond).
+namespace {
+struct PartitionSearch {
+    std::vector<int64_t> w;           // loads, descending
+    int g = 1;
+    int64_t lower = 0, best = 0;
+    std::vector<int> cur, best_asg;   // group of each item
+    std::vector<int64_t> load;
+    int64_t nodes = 0, budget = 20000000;
+    void dfs(size_t i, int64_t cur_max) {
+        if (best == lower || nodes > budget) return;
+        ++nodes;
+        if (i == w.size()) {
+            if (cur_max < best) { best = cur_max; best_asg = cur; }
+            return;
+        }
+        for (int q = 0; q < g; ++q) {
+            bool dup = false;             // a group with the same load was tried already
+            for (int p = 0; p < q; ++p)
+                if (load[p] == load[q]) { dup = true; break; }
+            if (dup) continue;
+            const int64_t nl = load[q] + w[i];
+            if (nl >= best) continue;
+            load[q] = nl;
+            cur[i] = q;
+            dfs(i + 1, std::max(cur_max, nl));
+            load[q] -= w[i];
+            if (best == lower || nodes > budget) return;
+        }
+    }
+};
+}  // namespace
+
 std::vector<std::vector<int>> partition(const std::vector<int>& nk, int g) {
-    int m = (int)nk.size();
+    const int m = (int)nk.size();
     std::vector<int> order(m);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nk[a] > nk[b]; });
-    std::vector<std::vector<int>> grp(g);
-    std::vector<int64_t> load(g, 0);
-    for (int i : order) {
-        int best = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        grp[best].push_back(i);
-        load[best] += nk[i] + 1;
+    PartitionSearch P;
+    P.g = std::max(1, g);
+    int64_t total = 0;
+    for (int i : order) { P.w.push_back(nk[i] + 1); total += nk[i] + 1; }
+    P.lower = m ? std::max<int64_t>((total + P.g - 1) / P.g, P.w[0]) : 0;
+    // LPT: the starting bound and the fallback
+    std::vector<int64_t> load(P.g, 0);
+    P.best_asg.assign(m, 0);
+    for (int j = 0; j < m; ++j) {
+        int q = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        P.best_asg[j] = q;
+        load[q] += P.w[j];
     }
-    bool improved = true;
-    while (improved) {
-        improved = false;
-        int hi = (int)(std::max_element(load.begin(), load.end()) - load.begin());
-        for (int o = 0; o < g && !improved; ++o) {
-            if (o == hi) continue;
-            for (size_t a = 0; a < grp[hi].size() && !improved; ++a) {
-                int ia = grp[hi][a];
-                // move
-                int64_t nh = load[hi] - (nk[ia] + 1), no = load[o] + (nk[ia] + 1);
-                if (std::max(nh, no) < load[hi]) {
-                    grp[o].push_back(ia); grp[hi].erase(grp[hi].begin() + a);
-                    load[hi] = nh; load[o] = no; improved = true; break;
-                }
-                for (size_t b = 0; b < grp[o].size(); ++b) {
-                    int ib = grp[o][b];
-                    int64_t d = (int64_t)nk[ia] - nk[ib];
-                    if (d > 0 && std::max(load[hi] - d, load[o] + d) < load[hi]) {
-                        std::swap(grp[hi][a], grp[o][b]);
-                        load[hi] -= d; load[o] += d; improved = true; break;
-                    }
-                }
-            }
-        }
+    P.best = m ? *std::max_element(load.begin(), load.end()) : 0;
+    if (P.best > P.lower) {
+        P.cur.assign(m, 0);
+        P.load.assign(P.g, 0);
+        P.dfs(0, 0);
     }
+    std::vector<std::vector<int>> grp(P.g);
+    for (int j = 0; j < m; ++j) grp[P.best_asg[j]].push_back(order[j]);
+    // deterministic group order: descending largest step count (empty groups last)
+    std::stable_sort(grp.begin(), grp.end(), [&](const std::vector<int>& a, const std::vector<int>& b) {
+        const int ma = a.empty() ? -1 : nk[a[0]], mb = b.empty() ? -1 : nk[b[0]];
+        return ma > mb;
+    });
     for (auto& v : grp) std::sort(v.begin(), v.end(), [&](int a, int b) { return nk[a] < nk[b]; });
     return grp;
 }

@@ -30,7 +30,9 @@ EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gb
            "gbs_bind_workspace", "gbs_bind_peers", "gbs_sync",
            "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
            "gbs_set_option",
-           "gbs_kernel_time", "gbs_strerror", "gbs_last_error"]
+           "gbs_kernel_time", "gbs_strerror", "gbs_last_error", "gbs_local_hub_create",
+           "gbs_local_hub_destroy"]
+GBS_TRANSPORT_NCCL, GBS_TRANSPORT_LOCAL = 0, 1
 
 
 class gbs_grid(ctypes.Structure):
@@ -40,7 +42,8 @@ class gbs_grid(ctypes.Structure):
 
 class gbs_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("groups", ctypes.c_int32), ("nccl_id", ctypes.c_uint8 * 128)]
+                ("groups", ctypes.c_int32), ("nccl_id", ctypes.c_uint8 * 128),
+                ("transport", ctypes.c_int32), ("pad", ctypes.c_int32), ("hub", ctypes.c_void_p)]
 
 
 class gbs_info(ctypes.Structure):
@@ -127,12 +130,15 @@ def load(build_if_missing: bool = False):
                                     ctypes.POINTER(gbs_halo_op), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     L.gbs_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     L.gbs_kernel_time.argtypes = [vp, ctypes.c_int, dp, ctypes.POINTER(i64), ctypes.c_int]
+    L.gbs_local_hub_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    L.gbs_local_hub_destroy.argtypes = [vp]
+    L.gbs_local_hub_destroy.restype = None
     L.gbs_strerror.argtypes = [ctypes.c_int]
     L.gbs_strerror.restype = ctypes.c_char_p
     L.gbs_last_error.argtypes = [vp]
     L.gbs_last_error.restype = ctypes.c_char_p
     for name in EXPORTS:
-        if name not in ("gbs_destroy", "gbs_strerror", "gbs_last_error"):  # int status
+        if name not in ("gbs_destroy", "gbs_strerror", "gbs_last_error", "gbs_local_hub_destroy"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -209,7 +215,10 @@ def gbs_create(pde: str, n: Sequence[int], stencil_order: int, n_k: Sequence[int
         dd = gbs_dist()
         dd.rank, dd.world = int(dist["rank"]), int(dist["world"])
         dd.device, dd.groups = int(dist.get("device", 0)), int(dist.get("groups", 0))
-        ctypes.memmove(dd.nccl_id, bytes(dist["nccl_id"]), 128)
+        if dist.get("nccl_id") is not None:
+            ctypes.memmove(dd.nccl_id, bytes(dist["nccl_id"]), 128)
+        dd.transport = int(dist.get("transport", GBS_TRANSPORT_NCCL))
+        dd.hub = dist.get("hub")
         dp = ctypes.pointer(dd)
     if stream is None:
         import torch
@@ -218,6 +227,45 @@ def gbs_create(pde: str, n: Sequence[int], stencil_order: int, n_k: Sequence[int
     _check(L.gbs_create(ctypes.byref(g), int(stencil_order), len(n_k), nk, wk, dp,
                         ctypes.c_void_p(int(stream) if stream else 0), ctypes.byref(out)))
     return out
+
+
+def gbs_local_hub_create(world: int, device: int = 0):
+    """In-process transport for `world` contexts on one device (include/gbs.h)."""
+    out = ctypes.c_void_p()
+    _check(load().gbs_local_hub_create(int(world), int(device), ctypes.byref(out)))
+    return out.value
+
+
+def gbs_local_hub_destroy(hub) -> None:
+    if hub:
+        load().gbs_local_hub_destroy(ctypes.c_void_p(hub))
+
+
+def run_local_ranks(world: int, fn, device: int = 0, groups: int = 0):
+    """Run fn(dist) for rank = 0..world-1 on `world` host threads, each rank a context of this
+    process on `device` joined through one local hub (GBS_TRANSPORT_LOCAL); returns the results in
+    rank order and re-raises the first exception.  Test/emulation harness: the ranks share a GPU."""
+    import threading
+    hub = gbs_local_hub_create(world, device)
+    res, err = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            res[r] = fn({"rank": r, "world": world, "device": device, "groups": groups,
+                         "transport": GBS_TRANSPORT_LOCAL, "hub": hub})
+        except BaseException as e:    # noqa: BLE001 - handed to the caller
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    gbs_local_hub_destroy(hub)
+    for e in err:
+        if e is not None:
+            raise e
+    return res
 
 
 def gbs_write_state(ctx, src) -> None:

@@ -1,0 +1,162 @@
+"""The multi-GPU path, executed: N ranks as N contexts of one process on one B200, joined
+by the in-process transport (GBS_TRANSPORT_LOCAL, include/gbs.h) and driven by N host
+threads.  Everything a rank does on N GPUs runs: gbs_create's communicator split, the
+sequence-group x slab plan, the per-group FE / LF / FIN0-FINACC chains, the per-substep
+halo schedule (matched in NCCL's posting order), the combine across sequence groups
+(PAPER.md:109-115 -- "the approximations ... are combined"; §3.6 folding, 388-400) and the
+slab all-gather of gbs_read_state.  Only the transport differs (device copies ordered by
+events instead of NCCL over NVLink; no kernel waits on another rank's kernel).
+
+Bar: every rank's full state within 1e-12 relative L2 of the oracle (per field and over all
+fields) and within 1e-12 RMS-relative max |error| per element; pure slabs (groups = 1) are
+bit-identical to the one-context run (same arithmetic per point; halos are exact copies).
+"""
+
+import numpy as np
+import pytest
+
+from gbs_inputs import get_config, make_ic, reduced
+from oracle import c_oracle as C
+from oracle import stability as S
+from oracle import weights as W
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1907_11771_b200 import gbs
+    gbs.load()
+    return torch
+
+
+def scheme_for(w, wset, cfg):
+    counts, ws, _ = W.scheme(wset, w.steps)
+    wd = W.to_double(ws)
+    H = S.macro_step_H(w.pde, w.order, w.n, counts, wd, w.h_factor)
+    # parity-only sets use min(H_config, 0.5 ISB(set)/rho) (reading R7)
+    cf, wf, _ = W.scheme(get_config(cfg).weights, w.steps)
+    H = min(H, S.macro_step_H(w.pde, w.order, w.n, cf, W.to_double(wf), w.h_factor))
+    return counts, wd, H
+
+
+def errors(got, ref):
+    """(max relative L2 over fields and all fields, max |err| / RMS(ref))."""
+    rel = [float(np.linalg.norm((got[f] - ref[f]).ravel()) / np.linalg.norm(ref[f].ravel()))
+           for f in range(ref.shape[0]) if np.linalg.norm(ref[f]) > 0]
+    rel.append(float(np.linalg.norm((got - ref).ravel()) / np.linalg.norm(ref.ravel())))
+    rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
+    return max(rel), float(np.max(np.abs(got - ref)) / rms)
+
+
+def run_ranks(torch, w, counts, wd, H, M, world, groups, opts=None):
+    from paper_1907_11771_b200 import gbs
+    y0 = make_ic(w)
+
+    def body(dist):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        with gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist, stream=s.cuda_stream,
+                         **(opts or {})) as st:
+            st.write(y0)
+            st.advance(M, H)
+            out = np.empty_like(y0)
+            st.read(out)
+            return out, st.info()
+
+    res = gbs.run_local_ranks(world, body, groups=groups)
+    return y0, [r[0] for r in res], [r[1] for r in res]
+
+
+def run_single(torch, w, counts, wd, H, M, opts=None):
+    from paper_1907_11771_b200 import gbs
+    y0 = make_ic(w)
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd, **(opts or {})) as st:
+        st.write(y0)
+        st.advance(M, H)
+        out = np.empty_like(y0)
+        st.read(out)
+    return out
+
+
+def check(torch, cfg, n, M, world, groups, wset="nonzero8", opts=None):
+    w = reduced(cfg, n, macro_steps=M, weights=wset)
+    counts, wd, H = scheme_for(w, wset, cfg)
+    y0, outs, infos = run_ranks(torch, w, counts, wd, H, M, world, groups, opts)
+    # the plan that ran: g groups x s slabs, every sequence in exactly one group
+    g = infos[0]["groups"]
+    assert g == groups and infos[0]["slabs"] == world // groups
+    seqs = {}
+    for r, info in enumerate(infos):
+        assert info["my_group"] * (world // groups) + info["my_slab"] == r
+        seqs[info["my_group"]] = info["my_substeps"]
+    assert sum(seqs.values()) == sum(k + 1 for k in counts)
+    # every rank gathered the same full state
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    ref = C.advance(w.pde, w.order, y0, counts, wd, H, M)
+    rel, mx = errors(outs[0], ref)
+    assert rel <= TOL and mx <= TOL, f"{cfg} {n} world={world} groups={groups}: rel L2 {rel:.3e}, max {mx:.3e}"
+    single = run_single(torch, w, counts, wd, H, M, opts)
+    if groups == 1:
+        assert np.array_equal(outs[0], single), "pure slabs must be bit-identical to one context"
+    else:
+        rel1, mx1 = errors(outs[0], single)
+        assert rel1 <= TOL and mx1 <= TOL
+    return rel, mx
+
+
+# 3-D wave, C4 scheme ({2..12}), two-substep TMA path (grid of whole 64 x 16 tiles)
+@pytest.mark.parametrize("world,groups", [(2, 1), (2, 2), (4, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4)])
+def test_wave3d_c4_scheme_tma(torch_cuda, world, groups):
+    check(torch_cuda, "c4", (64, 32, 48), 2, world, groups)
+
+
+# 3-D wave, C4 scheme, ragged grid (register kernels, odd x tail)
+@pytest.mark.parametrize("world,groups", [(2, 1), (2, 2), (4, 2), (8, 2)])
+def test_wave3d_c4_scheme_ragged(torch_cuda, world, groups):
+    check(torch_cuda, "c4", (70, 34, 48), 2, world, groups)
+
+
+# 3-D wave, C5 scheme ({2..16}), TMA path; slabs thick enough for the overlapped exchange
+@pytest.mark.parametrize("world,groups", [(2, 1), (4, 2), (4, 4), (8, 1), (8, 2), (8, 4)])
+def test_wave3d_c5_scheme_tma(torch_cuda, world, groups):
+    check(torch_cuda, "c5", (128, 16, 96), 2, world, groups)
+
+
+def test_wave3d_c5_scheme_fallback_weights(torch_cuda):
+    """The bench's weight set (zero weights on 10..16, sequences still run)."""
+    check(torch_cuda, "c5", (64, 16, 64), 2, 4, 2, wset="fallback8")
+
+
+# 2-D acoustics (slabs along y; p and v cross them): C2 (FD4) and C3 (FD8) schemes
+@pytest.mark.parametrize("cfg,n,world,groups", [("c3", (128, 64, 1), 2, 1), ("c3", (128, 64, 1), 2, 2),
+                                                ("c3", (128, 64, 1), 4, 2), ("c2", (96, 80, 1), 4, 1),
+                                                ("c2", (64, 128, 1), 8, 2), ("c3", (128, 96, 1), 4, 4)])
+def test_acoustic2d(torch_cuda, cfg, n, world, groups):
+    check(torch_cuda, cfg, n, 2, world, groups)
+
+
+# 1-D advection: sequence groups only (1-D grids are not slabbed)
+@pytest.mark.parametrize("world", [2, 4])
+def test_adv1d_groups(torch_cuda, world):
+    check(torch_cuda, "c1", (256, 1, 1), 5, world, world, wset="square8")
+
+
+@pytest.mark.parametrize("opts", [{"overlap": 0}, {"fuse": 0}, {"bulk": 0}])
+def test_wave3d_options_across_ranks(torch_cuda, opts):
+    """The exchange-then-compute path, single-substep kernels and register kernels across ranks."""
+    check(torch_cuda, "c4", (64, 32, 64), 2, 4, 2, opts=opts)
+
+
+def test_planner_choice_runs(torch_cuda):
+    """groups = 0: the planner's own choice for 8 ranks executes and matches the oracle."""
+    from paper_1907_11771_b200 import gbs
+    w = reduced("c5", (128, 16, 64), macro_steps=1, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8", "c5")
+    plan = gbs.gbs_plan(w.pde, w.n, w.order, counts, 8, 0, 0)
+    check(torch_cuda, "c5", (128, 16, 64), 1, 8, plan["groups"])
