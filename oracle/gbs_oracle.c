@@ -314,13 +314,16 @@ int oracle_advance(int pde, int order, const int64_t* dims, const double* scale,
         if (n_k[k] < 2 || (n_k[k] % 2) != 0) { release(&g); return -5; }
     if (!(H > 0.0)) { release(&g); return -6; }
     len = g.F * g.npts;
-    for (k = 0; k < 4; ++k) {
-        bufs[k] = (double*)malloc(sizeof(double) * (size_t)len);
-        if (!bufs[k]) return -7;
-    }
+    for (k = 0; k < 4; ++k) bufs[k] = (double*)malloc(sizeof(double) * (size_t)len);
     f = (double*)malloc(sizeof(double) * (size_t)len);
     acc = (double*)malloc(sizeof(double) * (size_t)len);
-    if (!f || !acc) return -7;
+    if (!bufs[0] || !bufs[1] || !bufs[2] || !bufs[3] || !f || !acc) {
+        for (k = 0; k < 4; ++k) free(bufs[k]);
+        free(f);
+        free(acc);
+        release(&g);
+        return -7;
+    }
 
     for (step = 0; step < M; ++step) {
         for (i = 0; i < len; ++i) acc[i] = 0.0;
@@ -356,23 +359,4 @@ int oracle_advance(int pde, int order, const int64_t* dims, const double* scale,
     free(acc);
     release(&g);
     return 0;
-}
-
-/*
- * One GBS component sequence on its own (Eq. (1) rows 1-3), no weighting:
- * out = y*_N for step count N from start Y.  Used by the tests that pin the
- * scalar stability function and the per-sequence pieces.
- */
-int oracle_component(int pde, int order, const int64_t* dims, const double* scale,
-                     int N, double H, const double* Y, double* out) {
-    int32_t nk = N;
-    double w = 1.0;
-    grid_t g;
-    int64_t len;
-    int rc = setup(&g, pde, order, dims, scale);
-    if (rc) return rc;
-    len = g.F * g.npts;
-    release(&g);
-    memcpy(out, Y, sizeof(double) * (size_t)len);
-    return oracle_advance(pde, order, dims, scale, 1, &nk, &w, H, 1, out);
 }

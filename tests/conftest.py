@@ -30,3 +30,12 @@ def _oracle_threads():
     except Exception:
         pass
     yield
+
+
+def record_parity(what, rel_l2, max_rel):
+    """Append one achieved parity margin to $GBS_PARITY_LOG (JSON lines), if set."""
+    path = os.environ.get("GBS_PARITY_LOG")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"case": what, "rel_l2": rel_l2, "max_abs_over_rms": max_rel}) + "\n")

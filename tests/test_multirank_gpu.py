@@ -20,6 +20,8 @@ from oracle import c_oracle as C
 from oracle import stability as S
 from oracle import weights as W
 
+from conftest import record_parity
+
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
@@ -100,6 +102,7 @@ def check(torch, cfg, n, M, world, groups, wset="nonzero8", opts=None):
         assert np.array_equal(o, outs[0])
     ref = C.advance(w.pde, w.order, y0, counts, wd, H, M)
     rel, mx = errors(outs[0], ref)
+    record_parity(f"multirank {cfg} {n} {wset} world={world} groups={groups} {opts or {}}", rel, mx)
     assert rel <= TOL and mx <= TOL, f"{cfg} {n} world={world} groups={groups}: rel L2 {rel:.3e}, max {mx:.3e}"
     single = run_single(torch, w, counts, wd, H, M, opts)
     if groups == 1:

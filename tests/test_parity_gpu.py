@@ -13,6 +13,8 @@ from oracle import c_oracle as C
 from oracle import stability as S
 from oracle import weights as W
 
+from conftest import record_parity
+
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
@@ -39,9 +41,15 @@ def rel_l2(a, b):
 
 
 def assert_parity(got, ref, tol=TOL, what=""):
+    """max relative L2 (per field and over all fields) <= tol, and per element
+    max |got - ref| / RMS(ref) <= tol (a single bad point cannot hide in the L2 norm)."""
     errs = [rel_l2(got[f], ref[f]) for f in range(ref.shape[0]) if np.linalg.norm(ref[f]) > 0]
     errs.append(rel_l2(got, ref))
+    rms = float(np.sqrt(np.mean(np.square(ref))))
+    mx = float(np.max(np.abs(got - ref)) / rms) if rms > 0 else float(np.max(np.abs(got - ref)))
+    record_parity(what, max(errs), mx)
     assert max(errs) <= tol, f"{what}: rel L2 per field/all = {errs}"
+    assert mx <= tol, f"{what}: max |err| / RMS = {mx:.3e}"
     for f in range(ref.shape[0]):
         if np.linalg.norm(ref[f]) == 0:
             assert np.max(np.abs(got[f])) <= tol * max(1.0, np.linalg.norm(ref) / np.sqrt(ref.size))
@@ -662,6 +670,55 @@ def test_c4_full_size_whole_run(torch_cuda):
 
 
 @pytest.mark.slow
+def test_c4_full_size_whole_run_nonzero_weights(torch_cuda):
+    """The whole C4 run (512^3, 10 macro steps) with the all-nonzero parity weights (SURVEY S3:
+    with fallback8 the sequences 10 and 12 carry w = 0, so a bug in them would be invisible)."""
+    w = get_config("c4").with_(weights="nonzero8")
+    counts, wd, H = scheme_for(get_config("c4"), "nonzero8")
+    gbs = gbs_mod()
+    y0 = make_ic(w)
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch_cuda.from_numpy(y0).cuda())
+        st.advance(w.macro_steps, H)
+        out = np.empty_like(y0)
+        st.read(out)
+    ref = C.advance(w.pde, w.order, y0, counts, wd, H, w.macro_steps)
+    assert_parity(out, ref, what="c4 full nonzero8, 10 macro steps")
+
+
+def _host_ram_gib():
+    try:
+        import psutil
+        return psutil.virtual_memory().total / 2**30
+    except Exception:
+        return 0.0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("wset", ["nonzero8", "fallback8"])
+def test_c5_scheme_full_state_at_bench_geometry(torch_cuda, wset):
+    """C5's scheme ({2..16}, FD8) over the WHOLE state of a 1024 x 1024 x nz grid in the bench's
+    launch geometry: the two-substep TMA kernel with 256-plane z-chunks (the automatic choice at
+    C5; forced here), 1024 x-y tiles per chunk.  nz = 512 (two chunks per column, 13.8 waves of
+    CTAs on 148 SMs) when the host has the RAM for the oracle, else 256.  One macro step = 80
+    substeps, 8 sequences, the C5 FE / LF-pair / LF+FIN0 / LF+FINACC launches."""
+    nz = 512 if _host_ram_gib() >= 160 else 256
+    w = get_config("c5").with_(n=(1024, 1024, nz), weights=wset)
+    counts, wd, H = scheme_for(get_config("c5"), wset)
+    gbs = gbs_mod()
+    y0 = make_ic(w)
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd, zchunk_pair=256) as st:
+        st.write(torch_cuda.from_numpy(y0).cuda())
+        st.advance(1, H)
+        out = np.empty_like(y0)
+        st.read(out)
+        launches = st.info()["kernel_launches"]
+    assert launches == sum(1 + k // 2 for k in counts)
+    ref = C.advance(w.pde, w.order, y0, counts, wd, H, 1)
+    assert_parity(out, ref, what=f"c5 scheme 1024x1024x{nz} {wset}, one macro step, 256-plane chunks")
+
+
+@pytest.mark.slow
 def test_c5_whole_run_conserves_means(torch_cuda):
     """Property at full size: the whole C5 run (1024^3, 4 macro steps). The zero Fourier mode
     of the 3-D wave evolves as u0' = v0, v0' = 0 with R(0)=1, R'(0)=sum w = 1, so the means of
@@ -685,12 +742,12 @@ def test_c5_whole_run_conserves_means(torch_cuda):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
-def test_3d_full_size_sampled(torch_cuda, cfg):
+@pytest.mark.parametrize("cfg,wset", [("c4", None), ("c5", None), ("c5", "nonzero8")])
+def test_3d_full_size_sampled(torch_cuda, cfg, wset):
     torch = torch_cuda
     gbs = gbs_mod()
     w = get_config(cfg)
-    counts, wd, H = scheme_for(w)
+    counts, wd, H = scheme_for(w, wset)
     y0 = make_ic(w)
     nx, ny, nz = w.n
     rng = np.random.default_rng(7)
