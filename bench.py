@@ -179,9 +179,21 @@ def describe(w, H):
 
 
 # ------------------------------------------------------------------------------ oracle timing
-def time_oracle_sample(w, counts, wd, H, target=1.0e9):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def time_oracle_sample(w, counts, wd, H, target=1.0e9, cores=None):
     """The oracle, as it stands, on a bounded sample of workload w: one macro step on a
-    grid shrunk (same PDE, stencil, scheme, H, IC recipe) to ~target pt-substeps."""
+    grid shrunk (same PDE, stencil, scheme, H, IC recipe) to ~target pt-substeps, on
+    `cores` OpenMP threads (default: every host core)."""
     import numpy as np
     from gbs_inputs import make_ic, reduced
     from oracle import c_oracle
@@ -197,7 +209,7 @@ def time_oracle_sample(w, counts, wd, H, target=1.0e9):
         n = w.n
     ws = reduced(w.name, n, macro_steps=1)
     y0 = make_ic(ws)
-    cores = os.cpu_count() or 1
+    cores = cores or os.cpu_count() or 1
     c_oracle.set_threads(cores)
     macro = 1 if w.ndim > 1 else 20
     t0 = time.perf_counter()
@@ -205,7 +217,7 @@ def time_oracle_sample(w, counts, wd, H, target=1.0e9):
     dt = time.perf_counter() - t0
     units = ws.points * S * macro
     grid = "x".join(str(v) for v in n[: w.ndim])
-    return {"value": units / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": units / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{macro} macro step(s) of the {w.name} scheme (same PDE, "
                       f"{'spectral' if w.order == 0 else 'FD%d' % w.order}, steps, "
                       f"weights, H) on a {grid} grid = {units:.3g} pt-substeps in {dt:.2f} s"}
@@ -287,8 +299,13 @@ def run_ours(a):
         # warm-up (also builds the CUDA graph when one is used)
         st.advance(a.warmup, H)
         gbs.gbs_sync(st.ctx)
+        # One step is one macro step, except on the whole-run cluster path (C1: a 2 KiB state,
+        # all macro steps of a gbs_advance in one launch), where one step is the config's whole
+        # run (w.macro_steps macro steps, one launch).
+        whole_run = w.ndim == 1 and a.warmup >= 1 and st.info()["kernel_launches"] == 1
+        run_len = w.macro_steps if whole_run else 1
         # Working sets that fit in L2 (C1, C2) are timed step by step with an L2 flush (a
-        # 512 MiB write) before every timed macro step; larger ones run back to back.
+        # 512 MiB write) before every timed step; larger ones run back to back.
         L2_BYTES = 126 * 2 ** 20
         flush = 6 * y0.nbytes < 2 * L2_BYTES
         scratch = torch.empty(64 * 2 ** 20, dtype=torch.float64, device=dev) if flush else None
@@ -299,7 +316,7 @@ def run_ours(a):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                st.advance(k, H)
+                st.advance(k * run_len, H)
                 e1.record(stream)
                 e1.synchronize()
                 return e0.elapsed_time(e1)
@@ -309,7 +326,7 @@ def run_ours(a):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                st.advance(1, H)
+                st.advance(run_len, H)
                 e1.record(stream)
                 evs.append((e0, e1))
             evs[-1][1].synchronize()
@@ -351,7 +368,7 @@ def run_ours(a):
         gbs.gbs_set_option(st.ctx, "time_kernels", 0)
 
     S = info["substeps_per_macro"]
-    units = w.points * S * a.steps
+    units = w.points * S * a.steps * run_len
     value = units / (ms * 1e-3)
     F = w.fields
     local_pts = w.points // max(1, info["slabs"])
@@ -362,7 +379,7 @@ def run_ours(a):
             2: ("final substep + averaging + weighted accumulate", 24 * F),
             3: ("two leap-frog substeps in one pass", 48 * F),
             4: ("leap-frog + final substep in one pass", 48 * F),
-            5: ("whole-run cluster kernel", 24 * F * S * a.steps)}
+            5: ("whole-run cluster kernel", 24 * F * S * run_len)}
     # bytes per point the kernel itself must read + write once (its own minimum HBM
     # traffic): the two-substep 3-D kernel moves S_u, U, S_v, P_v in and A_v, B, C_u out
     # (gbs_wave3d_pair.cuh) = 64 B instead of the metric's 2 x 24F = 96 B, and the FE
@@ -441,14 +458,19 @@ def run_ours(a):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = time_oracle_sample(w, counts, wd, H, target=8e9)       # ~10-30 s of CPU work
+        one = time_oracle_sample(w, counts, wd, H, target=5e8, cores=1)
+        cpu["one_core"] = {"value": one["value"], "sample": one["sample"]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
                 "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+                "macro_steps_per_step": run_len,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": describe(w, H), "grid": list(w.n[: w.ndim]), "fields": F,
                            "options": {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt},
-                           "substeps_per_step": S, "step": "1 macro step (all sequences + combine)",
+                           "substeps_per_step": S * run_len,
+                           "step": ("the whole %d-macro-step run in one cluster launch" % run_len if run_len > 1
+                                    else "1 macro step (all sequences + combine)"),
                            "l2": ("L2 flushed (512 MiB write) before every timed macro step: working set "
                                   "%.0f MiB < 2 x L2" % (6 * y0.nbytes / 2 ** 20) if flush else
                                   "inputs larger than L2 (each state buffer %.2f GiB)" % (y0.nbytes / 2 ** 30)),
@@ -462,11 +484,11 @@ def run_ours(a):
                                value * 24 * F / (8000.0 * 1e9 * world), 4)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "gpu_launches_per_rank": launches_rank,
-                "sim_time_per_s": H * a.steps / (ms * 1e-3),
+                "sim_time_per_s": H * a.steps * run_len / (ms * 1e-3),
                 "repeats": {"n": len(rep_ms),
-                            "values": [round(w.points * S * a.steps / (r * 1e-3), 1) for r in rep_ms],
-                            "median": w.points * S * a.steps / (statistics.median(rep_ms) * 1e-3),
-                            "best": w.points * S * a.steps / (min(rep_ms) * 1e-3)},
+                            "values": [round(units / (r * 1e-3), 1) for r in rep_ms],
+                            "median": units / (statistics.median(rep_ms) * 1e-3),
+                            "best": units / (min(rep_ms) * 1e-3)},
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -21,9 +21,13 @@
  *     GBS_ACOUSTIC2D  p_t = -(u_x + v_y), u_t = -p_x, v_t = -p_y    F = 3
  *     GBS_WAVE3D      u_t = v, v_t = u_xx + u_yy + u_zz             F = 2
  *
- * All arithmetic is IEEE fp64.  Every step above runs in this library's CUDA
- * kernels (sm_100a); there is no CPU fallback: without a usable CUDA device
- * gbs_create fails with GBS_E_CUDA.
+ * All arithmetic is IEEE fp64.  Every step above runs on the GPU, in this
+ * library's CUDA kernels (sm_100a) -- with one exception: the spectral
+ * derivative on grids beyond the cluster kernel (n[0] > 6400, or m > 16, or
+ * sequence groups across GPUs) transforms with cuFFT (D2Z / Z2D, a library
+ * call; the i k scaling and every substep update are this library's kernels).
+ * There is no CPU fallback: without a usable CUDA device gbs_create fails with
+ * GBS_E_CUDA.
  *
  * State layout (host or device, caller-owned): SoA fp64, [F][nz][ny][nx],
  * x fastest, unused axes of extent 1; count = F * nx * ny * nz values.

@@ -255,7 +255,10 @@ int gbs_bind_workspace(gbs_ctx* c, void* device_ptr, int64_t bytes) {
     c->have_state = false;              // the state must be written again
     c->peer_on = false;                 // peers are bound to a workspace
     c->peer_base[0] = c->peer_base[1] = nullptr;
-    if (device_ptr) CU(c, cudaMemset(static_cast<char*>(device_ptr) + state_bytes(c), 0, kPeerFlagBytes));
+    if (device_ptr) {
+        CU(c, cudaMemset(static_cast<char*>(device_ptr) + state_bytes(c), 0, kPeerFlagBytes));
+        c->peer_flags_fresh = true;
+    }
     return GBS_OK;
 }
 
@@ -277,7 +280,11 @@ int gbs_bind_peers(gbs_ctx* c, void* lower_workspace, void* upper_workspace) {
     for (auto& g : c->gexec) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     c->peer_base[0] = static_cast<char*>(lower_workspace);
     c->peer_base[1] = static_cast<char*>(upper_workspace);
-    c->peer_epoch = 0;
+    // epochs restart only over freshly zeroed flags (gbs_bind_workspace, then a cross-rank
+    // barrier by the caller before any rank binds); a re-bind keeps counting, so flags that
+    // still hold earlier epochs never satisfy a wait early
+    if (c->peer_flags_fresh) c->peer_epoch = 0;
+    c->peer_flags_fresh = false;
     c->peer_on = true;
     c->peer_ghosts_valid = false;
     return GBS_OK;

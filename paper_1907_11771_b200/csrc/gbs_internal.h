@@ -182,6 +182,7 @@ struct gbs_ctx {
     bool peer_on = false;
     bool peer_ghosts_valid = false;   // Y's ghost planes hold the neighbours' current face planes
     unsigned long long peer_epoch = 0;
+    bool peer_flags_fresh = false;    // this rank's flags were zeroed by gbs_bind_workspace
     char* peer_base[2] = {nullptr, nullptr};   // lower / upper neighbour's workspace (multi-GPU)
     unsigned long long* d_peer_flags = nullptr; // loopback: [slab][from lower, from upper]
     int band_opt = 0;                 // 3-D TMA tile launch order (0 = whole rows)

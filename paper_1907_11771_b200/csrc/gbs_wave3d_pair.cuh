@@ -161,6 +161,9 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     }
     __syncthreads();
     if (producer) {
+        // the TMA (async proxy) reads of peer-pushed ghost planes are ordered after the
+        // acquire by this thread's own proxy fence (the acquire ran on this thread too)
+        if constexpr (PEER) asm volatile("fence.proxy.async.global;" ::: "memory");
         prefetch_map(&M.su_a); prefetch_map(&M.su_b); prefetch_map(&M.su_c);
         prefetch_map(&M.u_a); prefetch_map(&M.u_b); prefetch_map(&M.u_c);
         prefetch_map(&M.sv); prefetch_map(&M.pv);
@@ -175,8 +178,9 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int64_t o = oz + own + (int64_t)r * nx;
-            const double2 su = __ldg(reinterpret_cast<const double2*>(A.Su + o));
-            const double2 uu = __ldg(reinterpret_cast<const double2*>(A.U + o));
+            // ghost planes may be peer-pushed memory: coherent loads (not .nc) under PEER
+            const double2 su = PEER ? ld_relaxed_sys2(A.Su + o) : __ldg(reinterpret_cast<const double2*>(A.Su + o));
+            const double2 uu = PEER ? ld_relaxed_sys2(A.U + o) : __ldg(reinterpret_cast<const double2*>(A.U + o));
             qs[j][2 * r] = su.x; qs[j][2 * r + 1] = su.y;
             qa[j][2 * r] = uu.x; qa[j][2 * r + 1] = uu.y;
         }

@@ -115,6 +115,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// coherent (not .nc) 128-bit load of memory other GPUs may write during the kernel
+__device__ __forceinline__ double2 ld_relaxed_sys2(const double* p) {
+    double2 v;
+    asm volatile("ld.relaxed.sys.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void peer_wait(const PeerPush& P) {
     const unsigned long long need = P.epoch - 1;
     while (ld_acquire_sys(P.wait_lo) < need || ld_acquire_sys(P.wait_hi) < need) __nanosleep(200);
@@ -208,6 +214,9 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
     if (ty == TY) {
         // ===================== producer warp =====================
         if (lane != 0) return;
+        // peer-pushed ghost planes: thread (0,0) acquired the neighbours' flags before the
+        // barrier; the TMA issuing thread orders its async-proxy reads after it itself
+        if constexpr (PEER) asm volatile("fence.proxy.async.global;" ::: "memory");
         prefetch_map(&M.su_a); prefetch_map(&M.su_b); prefetch_map(&M.su_c); prefetch_map(&M.sv);
         if constexpr (MODE != MODE_FE) { prefetch_map(&M.pu); prefetch_map(&M.pv); }
         if constexpr (MODE == MODE_FINACC) { prefetch_map(&M.au); prefetch_map(&M.av); }
@@ -259,7 +268,13 @@ wave3d_step_tma(const __grid_constant__ Maps M, const Wave3DArgs A, const int zb
     using V = Vec<2>;
     V q[2 * R + 1];
 #pragma unroll
-    for (int j = 0; j < R; ++j) q[j] = V::ld(A.Su + zoff(z0 - R + j) + own);   // planes z0-R .. z0-1
+    for (int j = 0; j < R; ++j)                  // planes z0-R .. z0-1 (coherent under PEER)
+        if constexpr (PEER) {
+            const double2 t = ld_relaxed_sys2(A.Su + zoff(z0 - R + j) + own);
+            q[j].v[0] = t.x; q[j].v[1] = t.y;
+        } else {
+            q[j] = V::ld(A.Su + zoff(z0 - R + j) + own);
+        }
     mbar_wait(init, 0);
 #pragma unroll
     for (int j = 0; j < R; ++j) {

@@ -32,10 +32,11 @@ def _oracle_threads():
     yield
 
 
-def record_parity(what, rel_l2, max_rel):
+def record_parity(what, rel_l2, max_over_rms, max_over_max=None):
     """Append one achieved parity margin to $GBS_PARITY_LOG (JSON lines), if set."""
     path = os.environ.get("GBS_PARITY_LOG")
     if not path:
         return
     with open(path, "a") as f:
-        f.write(json.dumps({"case": what, "rel_l2": rel_l2, "max_abs_over_rms": max_rel}) + "\n")
+        f.write(json.dumps({"case": what, "rel_l2": rel_l2, "max_abs_over_rms": max_over_rms,
+                            "max_abs_over_max": max_over_max}) + "\n")

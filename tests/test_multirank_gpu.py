@@ -8,7 +8,7 @@ slab all-gather of gbs_read_state.  Only the transport differs (device copies or
 events instead of NCCL over NVLink; no kernel waits on another rank's kernel).
 
 Bar: every rank's full state within 1e-12 relative L2 of the oracle (per field and over all
-fields) and within 1e-12 RMS-relative max |error| per element; pure slabs (groups = 1) are
+fields) and max |error| per element within 1e-11 of max |state|; pure slabs (groups = 1) are
 bit-identical to the one-context run (same arithmetic per point; halos are exact copies).
 """
 
@@ -24,6 +24,7 @@ from conftest import record_parity
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
+TOL_ELEM = 1e-11      # per element, relative to max |ref|
 
 
 @pytest.fixture(scope="module")
@@ -47,12 +48,13 @@ def scheme_for(w, wset, cfg):
 
 
 def errors(got, ref):
-    """(max relative L2 over fields and all fields, max |err| / RMS(ref))."""
+    """(max relative L2 over fields and all fields, max |err| / RMS(ref), max |err| / max |ref|)."""
     rel = [float(np.linalg.norm((got[f] - ref[f]).ravel()) / np.linalg.norm(ref[f].ravel()))
            for f in range(ref.shape[0]) if np.linalg.norm(ref[f]) > 0]
     rel.append(float(np.linalg.norm((got - ref).ravel()) / np.linalg.norm(ref.ravel())))
     rms = float(np.sqrt(np.mean(ref.astype(np.float64) ** 2)))
-    return max(rel), float(np.max(np.abs(got - ref)) / rms)
+    emax = float(np.max(np.abs(got - ref)))
+    return max(rel), emax / rms, emax / float(np.max(np.abs(ref)))
 
 
 def run_ranks(torch, w, counts, wd, H, M, world, groups, opts=None):
@@ -101,16 +103,16 @@ def check(torch, cfg, n, M, world, groups, wset="nonzero8", opts=None):
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
     ref = C.advance(w.pde, w.order, y0, counts, wd, H, M)
-    rel, mx = errors(outs[0], ref)
-    record_parity(f"multirank {cfg} {n} {wset} world={world} groups={groups} {opts or {}}", rel, mx)
-    assert rel <= TOL and mx <= TOL, f"{cfg} {n} world={world} groups={groups}: rel L2 {rel:.3e}, max {mx:.3e}"
+    rel, mrms, mmax = errors(outs[0], ref)
+    record_parity(f"multirank {cfg} {n} {wset} world={world} groups={groups} {opts or {}}", rel, mrms, mmax)
+    assert rel <= TOL and mmax <= TOL_ELEM, f"{cfg} {n} world={world} groups={groups}: rel L2 {rel:.3e}, max {mmax:.3e}"
     single = run_single(torch, w, counts, wd, H, M, opts)
     if groups == 1:
         assert np.array_equal(outs[0], single), "pure slabs must be bit-identical to one context"
     else:
-        rel1, mx1 = errors(outs[0], single)
-        assert rel1 <= TOL and mx1 <= TOL
-    return rel, mx
+        rel1, _, mmax1 = errors(outs[0], single)
+        assert rel1 <= TOL and mmax1 <= TOL_ELEM
+    return rel, mmax
 
 
 # 3-D wave, C4 scheme ({2..12}), two-substep TMA path (grid of whole 64 x 16 tiles)

@@ -17,6 +17,7 @@ from conftest import record_parity
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
+TOL_ELEM = 1e-11      # per element, relative to max |ref|
 
 
 @pytest.fixture(scope="module")
@@ -41,15 +42,18 @@ def rel_l2(a, b):
 
 
 def assert_parity(got, ref, tol=TOL, what=""):
-    """max relative L2 (per field and over all fields) <= tol, and per element
-    max |got - ref| / RMS(ref) <= tol (a single bad point cannot hide in the L2 norm)."""
+    """max relative L2 (per field and over all fields) <= tol (north_star's bar), and per
+    element max |got - ref| <= TOL_ELEM * max |ref| (a single wrong point cannot
+    hide in the L2 norm of a large grid; rounding reaches ~1e-12 of the maximum, a wrong
+    coefficient, halo plane or dropped term >= 1e-6)."""
     errs = [rel_l2(got[f], ref[f]) for f in range(ref.shape[0]) if np.linalg.norm(ref[f]) > 0]
     errs.append(rel_l2(got, ref))
+    amax = float(np.max(np.abs(ref)))
+    emax = float(np.max(np.abs(got - ref)))
     rms = float(np.sqrt(np.mean(np.square(ref))))
-    mx = float(np.max(np.abs(got - ref)) / rms) if rms > 0 else float(np.max(np.abs(got - ref)))
-    record_parity(what, max(errs), mx)
+    record_parity(what, max(errs), emax / rms if rms > 0 else emax, emax / amax if amax > 0 else emax)
     assert max(errs) <= tol, f"{what}: rel L2 per field/all = {errs}"
-    assert mx <= tol, f"{what}: max |err| / RMS = {mx:.3e}"
+    assert emax <= TOL_ELEM * max(amax, 1e-300), f"{what}: max |err| / max |ref| = {emax / amax:.3e}"
     for f in range(ref.shape[0]):
         if np.linalg.norm(ref[f]) == 0:
             assert np.max(np.abs(got[f])) <= tol * max(1.0, np.linalg.norm(ref) / np.sqrt(ref.size))
