@@ -280,6 +280,16 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *   "bulk"         1/0   TMA-pipelined 3-D kernels on grids that are multiples of
  *                        their 64 x 16 tile (default 1; 0 = register-prefetch kernels)
  *   "fuse"         1/0   two substeps per HBM pass on 3-D TMA grids (default 1)
+ *   "half"         1/0   3-D TMA grids: each two-substep leap-frog pass as two launches of the
+ *                        single-stencil-field kernel (half A: v_{n+1}, u_{n+2} from P_v, S_u; half B:
+ *                        v_{n+2}, u_{n+3} from S_v, U -- the two share no value), 64 x 32 tiles,
+ *                        one register queue per CTA (default 1; 0 = the coupled pair kernel;
+ *                        peer pushes always use the coupled kernel)
+ *   "half_fe"      1/0   the forward-Euler substep through the same kernel (default 1)
+ *   "half_tall"    1/0   64 x 32 tiles for the half kernel when ny % 32 == 0 (default 1)
+ *   "half_rpt"     2/4   rows per thread of the tall half kernel (16 or 8 consumer warps; default 2)
+ *   "l2hint_half"  bits  half kernel: 1 centre boxes evict_last, 2 streaming loads of the
+ *                        pointwise field, 4 halo boxes evict_first, 8 streaming stores (default 11)
  *   "fuse2d"       1/0   2-D acoustics: two substeps per pass as the chain-U / chain-P
  *                        kernel pair (default 0: bit-identical but measured slower
  *                        than single substeps on B200)
@@ -310,7 +320,8 @@ GBS_API int gbs_set_option(gbs_ctx* ctx, const char* key, int64_t value);
 /* Accumulated device time (ms) and launch count of the timed kernels of a class
  * since the last reset: cls 0 = interior LF, 1 = FE, 2 = final (average + weighted
  * accumulate), 3 = two LF substeps in one pass, 4 = LF + final in one pass, 5 = the
- * whole-run cluster kernel.  reset = 1 clears the counters after reading. */
+ * whole-run cluster kernel, 6 = one single-stencil-field half of a two-substep pass
+ * (option "half").  reset = 1 clears the counters after reading. */
 GBS_API int gbs_kernel_time(gbs_ctx* ctx, int cls, double* total_ms, int64_t* launches, int reset);
 
 GBS_API const char* gbs_strerror(int code);

@@ -179,6 +179,14 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "bulk") { c->use_bulk = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse") { c->use_fuse = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fuse2d") { c->use_fuse2d = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "half") { c->use_half = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "half_fe") { c->half_fe = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "half_tall") { c->half_tall = value != 0; drop_graphs(); return GBS_OK; }
+    if (k == "half_rpt") {
+        if (value != 2 && value != 4) return fail(c, GBS_E_INVAL, "half_rpt must be 2 or 4");
+        c->half_rpt = (int)value; drop_graphs(); return GBS_OK;
+    }
+    if (k == "l2hint_half") { c->hint_half_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "loopback_nccl") {
         if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback_nccl needs a single-GPU context");
         const bool on = value != 0;
@@ -318,7 +326,7 @@ int gbs_query(const gbs_ctx* c, gbs_info* info) {
 }
 
 int gbs_kernel_time(gbs_ctx* c, int cls, double* total_ms, int64_t* launches, int reset) {
-    if (!c || cls < 0 || cls > 5) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
+    if (!c || cls < 0 || cls > 7) return fail(c, GBS_E_INVAL, "ctx NULL or cls out of range");
     int rc = harvest_timer(c);
     if (rc) return rc;
     if (total_ms) *total_ms = c->timer.total_ms[cls];

@@ -13,6 +13,7 @@
 #include "gbs_internal.h"
 #include "gbs_wave3d_tma.cuh"     // substep modes and the TMA tile (no launches here)
 #include "gbs_acoustic2d_pair.cuh"  // AC2_BH (band rows of the 2-D chain kernels)
+#include "gbs_wave3d_half.cuh"      // HALF_LF / HALF_FE
 
 // ---------------------------------------------------------------------------
 // halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
@@ -222,6 +223,18 @@ static int pair_step(gbs_ctx* c, int cls, const PairOperands& op) {
     return GBS_OK;
 }
 
+// one single-stencil-field launch (gbs_wave3d_half.cuh): the halo of X is read
+static int half_step(gbs_ctx* c, int cls, const HalfOperands& op) {
+    int rc;
+    cudaEvent_t end = nullptr;
+    if (c->time_kernels && (rc = timed_begin(c, cls, &end))) return rc;
+    rc = run_overlapped(c, [&](Slab& s, int64_t lo, int64_t hi, int64_t gap) { return launch_half(c, s, op, lo, hi, gap); },
+                        {{op.X.b, 1u << op.X.f}});
+    if (rc) return rc;
+    if (end) CU(c, cudaEventRecord(end, c->stream));
+    return GBS_OK;
+}
+
 // 2-D acoustics: two leap-frog substeps per pass (two chain kernels); they read S (p, u, v)
 // and P (p, v) with y stencils
 static int ac2d_pair_step(gbs_ctx* c, int cls, int P, int S, int Aout, int Bout, double cfA, double cfB) {
@@ -299,17 +312,35 @@ static int enqueue_macro(gbs_ctx* c, double H) {
             // (LF1, LF2), ..., (LF_{n-1}, final).  Field slots: y1 -> buffer 2; the
             // u-levels rotate through (2,0)/(3,0) and (4,0)/(5,0); v_{odd} stays in
             // (2,1) and v_{even} in (3,1), both updated in place (pointwise reads).
-            StepOperands fe{Y, Y, 2, gbs::MODE_FE, h, 0.0, false};
-            fe.xu = Slot{3, 0};
-            fe.cf2 = 2.0 * h;
-            if ((rc = step(c, 1, fe))) return rc;                                            // y1, u2
+            const bool half = half_eligible(c);
+            if (half && c->half_fe) {
+                // v1 = v0 + h lap(u0), u2 = u0 + 2h v1, u1 = u0 + h v0 (the FE kernel's values)
+                HalfOperands fe{gbs::tma::HALF_FE, Slot{Y, 0}, Slot{Y, 1}, Slot{2, 1}, Slot{3, 0}, Slot{2, 0},
+                                h, 2.0 * h};
+                if ((rc = half_step(c, 1, fe))) return rc;
+            } else {
+                StepOperands fe{Y, Y, 2, gbs::MODE_FE, h, 0.0, false};
+                fe.xu = Slot{3, 0};
+                fe.cf2 = 2.0 * h;
+                if ((rc = step(c, 1, fe))) return rc;                                        // y1, u2
+            }
             Slot Pv{Y, 1}, Su{2, 0}, Sv{2, 1}, U{3, 0};
             for (int p = 0; p < n / 2; ++p) {
                 if (p + 1 < n / 2) {
                     const int nb = Su.b == 2 ? 4 : 2;
                     PairOperands op{Pv, Su, Sv, U, Slot{3, 1}, Slot{nb, 0}, Sv, Slot{nb + 1, 0},
                                     gbs::MODE_LF, 2.0 * h, 2.0 * h, 0.0, false};
-                    if ((rc = pair_step(c, 3, op))) return rc;
+                    if (half) {
+                        // the pair's two independent halves (gbs_wave3d_half.cuh): neither reads
+                        // what the other writes
+                        HalfOperands ha{gbs::tma::HALF_LF, op.Su, op.Pv, op.Av, op.Bu};
+                        ha.c1 = op.cfA; ha.c2 = op.cfB;
+                        HalfOperands hb{gbs::tma::HALF_LF, op.U, op.Sv, op.Bv, op.Cu};
+                        hb.c1 = op.cfB; hb.c2 = op.cfA;
+                        if ((rc = half_step(c, 6, ha)) || (rc = half_step(c, 6, hb))) return rc;
+                    } else if ((rc = pair_step(c, 3, op))) {
+                        return rc;
+                    }
                     Pv = Slot{3, 1}; Su = Slot{nb, 0}; U = Slot{nb + 1, 0};
                 } else {
                     PairOperands fin{Pv, Su, Sv, U, Slot{ACC, 0}, Slot{ACC, 0}, Slot{ACC, 1}, Slot{ACC, 0},

@@ -110,8 +110,8 @@ struct KernelTimer {
     std::vector<cudaEvent_t> ev;      // pairs
     std::vector<int> cls;
     size_t used = 0;
-    double total_ms[6] = {0, 0, 0, 0, 0, 0};
-    int64_t launches[6] = {0, 0, 0, 0, 0, 0};
+    double total_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t launches[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 struct gbs_ctx {
@@ -176,6 +176,12 @@ struct gbs_ctx {
     int zchunk_pair_opt = 0;          // planes per CTA of the two-substep kernel (0 = zchunk, else 256)
     int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
     int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
+    bool use_half = true;             // leap-frog pairs as two single-stencil-field launches, FE
+                                      // through the same kernel (gbs_wave3d_half.cuh)
+    bool half_tall = true;            // 64 x 32 tiles when ny allows
+    int half_rpt = 2;                 // rows per thread of the tall half kernel (2 or 4)
+    bool half_fe = true;              // FE through the half kernel
+    int hint_half_opt = 11;           // half kernel L2 / streaming bits (HalfArgs::hint)
     bool loop_nccl = false;           // loopback halos through NCCL on a one-rank communicator
     // peer halo pushes (gbs_wave3d_tma.cuh PeerPush): option "peer" (loopback slabs) or
     // gbs_bind_peers (one slab per GPU, neighbours' workspaces mapped into this process)
@@ -247,6 +253,15 @@ struct PairOperands {
     bool flag;
 };
 
+// One single-stencil-field 3-D launch (gbs_wave3d_half.cuh): O1 = P + c1 lap(X),
+// O2 = X + c2 O1 (+ O3 = X + c1 P for the forward-Euler kind).
+struct HalfOperands {
+    int kind;             // gbs::tma::HALF_LF or HALF_FE
+    Slot X, P, O1, O2;
+    Slot O3 = {-1, 0};
+    double c1 = 0.0, c2 = 0.0;
+};
+
 // ---- gbs_plan.cu
 std::vector<std::vector<int>> partition(const std::vector<int>& nk, int g);
 int64_t crit_path(const std::vector<int>& nk, int g);
@@ -262,6 +277,8 @@ void free_state(gbs_ctx* c);
 // [lo, hi) of slab s; gap > 0: only the two face bands of (hi - lo - gap) / 2 planes each
 int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t hi, int64_t gap = 0);
 int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi, int64_t gap = 0);
+int launch_half(gbs_ctx* c, Slab& s, const HalfOperands& op, int64_t lo, int64_t hi, int64_t gap = 0);
+bool half_eligible(const gbs_ctx* c);
 // ghost rows of a single slab from its own opposite side, for (buffer, field mask) pairs
 int launch_ghost_fill(gbs_ctx* c, const std::vector<std::pair<int, unsigned>>& halos);
 // 2-D acoustics, two leap-frog substeps (P, S buffers -> A = y_{n+1}, B = y_{n+2} buffers)

@@ -10,6 +10,7 @@
 #include "gbs_kernels.cuh"
 #include "gbs_wave3d_tma.cuh"
 #include "gbs_wave3d_pair.cuh"
+#include "gbs_wave3d_half.cuh"
 #include "gbs_acoustic2d_tma.cuh"
 #include "gbs_acoustic2d_pair.cuh"
 #include "gbs_adv1d_cluster.cuh"
@@ -123,6 +124,9 @@ int ensure_buffers(gbs_ctx* c) {
                     ok = make_map(&s.tm[b][f][0], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TY) &&
                          make_map(&s.tm[b][f][1], base, c->n[0], vy, vz, gbs::tma::TX, c->R) &&
                          make_map(&s.tm[b][f][2], base, c->n[0], vy, vz, c->R, gbs::tma::TY);
+                    if (ok && c->pde == GBS_WAVE3D && c->n[1] % gbs::tma::TYH_TALL == 0)   // half kernel, tall tiles
+                        ok = make_map(&s.tm[b][f][3], base, c->n[0], vy, vz, gbs::tma::TX, gbs::tma::TYH_TALL) &&
+                             make_map(&s.tm[b][f][4], base, c->n[0], vy, vz, c->R, gbs::tma::TYH_TALL);
                     if (ok && c->pde == GBS_ACOUSTIC2D) {   // the chain kernels' boxes (Ac2PairMaps)
                         const int BH = gbs::tma::AC2_BH;
                         ok = make_map(&s.tm[b][f][3], base, c->n[0], vy, vz, gbs::tma::TX, BH) &&
@@ -526,6 +530,77 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     else { if (slab) { PR(4, true) } else { PR(4, false) } }
 #undef PR
     if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "pair kernel setup: %s", cudaGetErrorString(e));
+    c->launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return GBS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// single-stencil-field 3-D kernel (gbs_wave3d_half.cuh): one half of a leap-frog pair,
+// or the forward-Euler substep, over the planes [lo, hi) of slab s
+// ---------------------------------------------------------------------------
+template <int R, int KIND, bool SLAB, int TYH, int RPT>
+static cudaError_t launch_half_tma(const gbs::tma::HalfMaps& m, const gbs::tma::HalfArgs& a, int zbase, dim3 grid,
+                                   cudaStream_t st) {
+    constexpr int D = gbs::tma::HALF_D;
+    using L = gbs::tma::HalfLayout<R, TYH, D>;
+    auto k = gbs::tma::wave3d_half_tma<R, KIND, SLAB, TYH, RPT, D>;
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), L::bytes);
+    if (e != cudaSuccess) return e;
+    k<<<grid, dim3(32, TYH / RPT), L::bytes, st>>>(m, a, zbase);
+    return cudaSuccess;
+}
+
+bool half_eligible(const gbs_ctx* c) {
+    return c->pde == GBS_WAVE3D && c->use_half && c->tma_grid && !c->peer_on;
+}
+
+int launch_half(gbs_ctx* c, Slab& s, const HalfOperands& op, int64_t lo, int64_t hi, int64_t gap) {
+    const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
+    const bool tall = c->n[1] % gbs::tma::TYH_TALL == 0 && c->half_tall;
+    const int TYH = tall ? gbs::tma::TYH_TALL : gbs::tma::TY;
+    const int rpt = tall && c->half_rpt == 4 ? 4 : 2;
+    gbs::tma::HalfArgs a{};
+    a.X = field_ptr(c, s, op.X.b, op.X.f);
+    a.P = field_ptr(c, s, op.P.b, op.P.f);
+    a.O1 = field_ptr(c, s, op.O1.b, op.O1.f);
+    a.O2 = field_ptr(c, s, op.O2.b, op.O2.f);
+    a.O3 = op.kind == gbs::tma::HALF_FE ? field_ptr(c, s, op.O3.b, op.O3.f) : nullptr;
+    a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
+    a.plane = c->plane;
+    const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
+    a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
+    a.c1 = op.c1; a.c2 = op.c2;
+    a.zlo = (int)lo; a.zhi = (int)hi;
+    const int64_t tiles = (c->n[0] / gbs::tma::TX) * (c->n[1] / TYH);
+    const int zauto = tiles * ((hi - lo + 255) / 256) >= 8LL * c->sms ? 256 : 128;
+    const int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : zauto;
+    a.zchunk = (int)std::min<int64_t>(zc, hi - lo);
+    a.band = tile_band(c, c->n[0] / gbs::tma::TX);
+    a.hint = c->hint_half_opt;
+    dim3 grid((unsigned)tiles, 1u, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
+    face_chunks(lo, hi, gap, a.zchunk, a.zskip, grid.z);
+    gbs::tma::HalfMaps m;
+    m.x_a = s.tm[op.X.b][op.X.f][tall ? 3 : 0];
+    m.x_b = s.tm[op.X.b][op.X.f][1];
+    m.x_c = s.tm[op.X.b][op.X.f][tall ? 4 : 2];
+    const int zbase = (int)c->ghost;
+    cudaError_t e = cudaSuccess;
+#define HL(RR, SL)                                                                                                   \
+    if (op.kind == gbs::tma::HALF_FE) {                                                                              \
+        if (!tall) e = launch_half_tma<RR, gbs::tma::HALF_FE, SL, gbs::tma::TY, 2>(m, a, zbase, grid, c->stream);     \
+        else if (rpt == 4) e = launch_half_tma<RR, gbs::tma::HALF_FE, SL, gbs::tma::TYH_TALL, 4>(m, a, zbase, grid, c->stream); \
+        else e = launch_half_tma<RR, gbs::tma::HALF_FE, SL, gbs::tma::TYH_TALL, 2>(m, a, zbase, grid, c->stream);    \
+    } else {                                                                                                         \
+        if (!tall) e = launch_half_tma<RR, gbs::tma::HALF_LF, SL, gbs::tma::TY, 2>(m, a, zbase, grid, c->stream);     \
+        else if (rpt == 4) e = launch_half_tma<RR, gbs::tma::HALF_LF, SL, gbs::tma::TYH_TALL, 4>(m, a, zbase, grid, c->stream); \
+        else e = launch_half_tma<RR, gbs::tma::HALF_LF, SL, gbs::tma::TYH_TALL, 2>(m, a, zbase, grid, c->stream);    \
+    }
+    if (c->R == 2) { if (slab) { HL(2, true) } else { HL(2, false) } }
+    else { if (slab) { HL(4, true) } else { HL(4, false) } }
+#undef HL
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "half kernel setup: %s", cudaGetErrorString(e));
     c->launches++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));

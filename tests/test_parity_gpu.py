@@ -200,6 +200,35 @@ def test_two_substep_kernel_bitwise_equals_single_steps(torch_cuda, cfg, n):
     assert ia["kernel_launches"] == 2 * sum(1 + k // 2 for k in counts)
 
 
+@pytest.mark.parametrize("cfg,n,opts", [
+    ("c5", (128, 64, 40), {}),                                    # 64 x 32 tiles, 16 warps
+    ("c5", (128, 64, 40), {"half_rpt": 4}),                       # 64 x 32 tiles, 8 warps
+    ("c4", (64, 48, 30), {}),                                     # ny % 32 != 0: 64 x 16 tiles
+    ("c4", (128, 32, 24), {"half_tall": 0}),
+    ("c5", (64, 64, 48), {"loopback": 3}),                        # slabs, overlapped exchange
+    ("c5", (64, 32, 40), {"loopback": 2, "overlap": 0, "graph": 0}),
+    ("c4", (64, 32, 24), {"half_fe": 0}),                         # FE through the step kernel
+    ("c5", (64, 32, 40), {"l2hint_half": 0, "zchunk_pair": 7}),   # no cache hints, ragged z chunks
+    ("c4", (64, 16, 9), {}),                                      # nz = 2r + 1
+])
+def test_half_kernels_bitwise_equal_coupled_pair(torch_cuda, cfg, n, opts):
+    """Leap-frog pairs as two single-stencil-field launches (gbs_wave3d_half.cuh, option "half"),
+    the FE through the same kernel: the same operations in the same order as the coupled pair
+    kernel and the FE step kernel -> bit-identical results, and the oracle's within 1e-12."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, half=1))
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, half=0))
+    assert np.array_equal(a[0], b[0])
+    slabs = opts.get("loopback", 1)
+    pairs = sum(k // 2 - 1 for k in counts)                       # LF pairs per macro step
+    # per macro step and slab: one more launch per LF pair (plus, with overlap, its face band)
+    per_pair = 1 if (slabs == 1 or not opts.get("overlap", 1)) else 2
+    assert ia["kernel_launches"] - ib["kernel_launches"] == 2 * slabs * pairs * per_pair
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(a[0], o[0], what=f"half kernels {cfg} {n} {opts}")
+
+
 @pytest.mark.parametrize("opts", [{"band": 1}, {"band": 2}, {"band": 3}, {"l2hint": 0},
                                   {"l2hint": 15, "l2hint_step": 11}])
 def test_tile_order_and_cache_policies_do_not_change_results(torch_cuda, opts):
@@ -799,6 +828,7 @@ def _random_cases(seed=20261020, count=14, include_1d=False):
         lbs = [s for s in (1, 2, 3, 4) if slow % s == 0 and slow // s >= R]
         lb = int(rng.choice(lbs))
         opts = {"loopback": lb, "overlap": int(rng.integers(0, 2)), "graph": int(rng.integers(0, 2)),
+                "half": int(rng.integers(0, 2)), "half_rpt": int(rng.choice([2, 4])),
                 "fuse": int(rng.integers(0, 2)), "band": int(rng.choice([0, 1, 2])),
                 "zchunk": int(rng.choice([0, 0, 8, 17])), "zchunk_pair": int(rng.choice([0, 0, 5, 32])),
                 "l2hint": int(rng.choice([11, 0, 15]))}
