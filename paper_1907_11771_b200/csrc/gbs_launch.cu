@@ -543,7 +543,7 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
 template <int R, int KIND, bool SLAB, int TYH, int RPT>
 static cudaError_t launch_half_tma(const gbs::tma::HalfMaps& m, const gbs::tma::HalfArgs& a, int zbase, dim3 grid,
                                    cudaStream_t st) {
-    constexpr int D = gbs::tma::HALF_D;
+    constexpr int D = TYH == gbs::tma::TY ? 4 : 3;
     using L = gbs::tma::HalfLayout<R, TYH, D>;
     auto k = gbs::tma::wave3d_half_tma<R, KIND, SLAB, TYH, RPT, D>;
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), L::bytes);
@@ -585,6 +585,7 @@ int launch_half(gbs_ctx* c, Slab& s, const HalfOperands& op, int64_t lo, int64_t
     m.x_a = s.tm[op.X.b][op.X.f][tall ? 3 : 0];
     m.x_b = s.tm[op.X.b][op.X.f][1];
     m.x_c = s.tm[op.X.b][op.X.f][tall ? 4 : 2];
+    m.p = s.tm[op.P.b][op.P.f][tall ? 3 : 0];
     const int zbase = (int)c->ghost;
     cudaError_t e = cudaSuccess;
 #define HL(RR, SL)                                                                                                   \

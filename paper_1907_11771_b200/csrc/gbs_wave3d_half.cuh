@@ -26,8 +26,10 @@
 //     kernel) and the halo loads per point;
 //   * the queue front (plane z + R) comes from a ring of R + D tiles instead of a
 //     second TMA box of the same data;
-//   * the pointwise field P is read by the consumer threads with streaming 128-bit
-//     global loads two planes ahead (no shared-memory round trip);
+//   * the pointwise field P arrives by TMA in the same stage as the tile (a version that
+//     read it with register-prefetched global loads exposed their latency: 56% of the
+//     stall samples long-scoreboard on the register move at the loop top, ncu; double
+//     buffering it in registers spilled);
 //   * 16 warps (RPT = 2 rows x 2 columns per thread) or 8 (RPT = 4).
 // Producer: lane 0 of warp 0 issues the five boxes of plane z + R + D - 1 (centre
 // TX x TYH, y halos TX x R, x strips R x TYH) into a ring of R + D tiles through
@@ -41,7 +43,6 @@ namespace tma {
 
 enum { HALF_LF = 0, HALF_FE = 1 };
 constexpr int TYH_TALL = 32;           // tile rows on grids with ny % 32 == 0
-constexpr int HALF_D = 4;              // TMA stages ahead of the queue front
 
 template <int R, int TYH, int D>
 struct HalfLayout {
@@ -50,14 +51,18 @@ struct HalfLayout {
     static constexpr int STRIP = TYH * R;
     static constexpr int TILE = CENTER + 2 * STRIP;
     static constexpr int RING = R + D;
+    static constexpr int PWT = TYH * TX;                  // one plane of the pointwise field P
     static constexpr size_t ring_doubles = (size_t)RING * TILE;
-    static constexpr size_t bytes = ring_doubles * 8 + (2 * D + 1) * 8;
+    static constexpr size_t p_doubles = (size_t)D * PWT;
+    static constexpr size_t bytes = (ring_doubles + p_doubles) * 8 + (2 * D + 1) * 8;
     static constexpr uint32_t tile_bytes = TILE * 8;
+    static constexpr uint32_t stage_bytes = (TILE + PWT) * 8;
     static_assert((CENTER * 8) % 128 == 0 && (STRIP * 8) % 128 == 0, "TMA destinations need 128 B alignment");
 };
 
 struct HalfMaps {
     CUtensorMap x_a, x_b, x_c;        // X: TX x TYH centre, TX x R y halos, R x TYH x strips
+    CUtensorMap p;                    // P: TX x TYH
 };
 
 struct HalfArgs {
@@ -70,7 +75,7 @@ struct HalfArgs {
     double sx2, sy2, sz2;
     double c1, c2;
     int band;
-    int hint;                         // 1 centre boxes evict_last, 2 P streaming loads,
+    int hint;                         // 1 centre boxes evict_last, 2 P box evict_first,
                                       // 4 halo boxes evict_first, 8 streaming stores
 };
 
@@ -80,10 +85,10 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
     using L = HalfLayout<R, TYH, D>;
     constexpr int NW = TYH / RPT;              // warps; lane 0 of warp 0 also issues the TMA boxes
     constexpr int RING = L::RING, TILE = L::TILE;
-    constexpr int PF = RPT == 2 ? 1 : 2;       // planes of P loaded ahead
     extern __shared__ __align__(128) double smem[];
     double* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::ring_doubles);
+    double* pst = smem + L::ring_doubles;      // P of plane i in slot i % D
+    uint64_t* full = reinterpret_cast<uint64_t*>(pst + L::p_doubles);
     uint64_t* empty = full + D;
     uint64_t* init = empty + D;
 
@@ -121,8 +126,9 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
     auto issue_stage = [&](int k) {
         const int s = k % D;
         if (k >= D) mbar_wait(&empty[s], (uint32_t)(((k / D) - 1) & 1));
-        mbar_expect_tx(&full[s], L::tile_bytes);
+        mbar_expect_tx(&full[s], L::stage_bytes);
         issue_tile(k + R, &full[s]);
+        ld(pst + (size_t)s * L::PWT, &M.p, x0, y0, zc(z0 + k), &full[s], 2, pol_first);   // P of plane k
     };
     if (producer) {
         for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
@@ -131,7 +137,7 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
     }
     __syncthreads();
     if (producer) {
-        prefetch_map(&M.x_a); prefetch_map(&M.x_b); prefetch_map(&M.x_c);
+        prefetch_map(&M.x_a); prefetch_map(&M.x_b); prefetch_map(&M.x_c); prefetch_map(&M.p);
         mbar_expect_tx(init, R * L::tile_bytes);
         for (int p = 0; p < R; ++p) issue_tile(p, init);
         for (int k = 0; k < D - 1 && k < niter; ++k) issue_stage(k);
@@ -144,21 +150,7 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
         if constexpr (SLAB) return (int64_t)z * plane;
         else return (int64_t)wrap_once(z, nz) * plane;
     };
-    const bool pcs = A.hint & 2, scs = A.hint & 8;
-    auto ldp = [&](const double* p) -> double2 {
-        return pcs ? __ldcs(reinterpret_cast<const double2*>(p)) : __ldg(reinterpret_cast<const double2*>(p));
-    };
-    // P of planes z0 .. z0 + PF - 1 (planes beyond the chunk are clamped into it, never used)
-    double pp[PF][RPT][2];
-#pragma unroll
-    for (int k = 0; k < PF; ++k) {
-        const int zk = z0 + min(k, niter - 1);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-            const double2 t = ldp(A.P + zoff(zk) + own + (int64_t)r * nx);
-            pp[k][r][0] = t.x; pp[k][r][1] = t.y;
-        }
-    }
+    const bool scs = A.hint & 8;
     // register queue of X at planes z - R .. z + R; point (row r, column v) -> [r][v]
     double q[2 * R + 1][RPT][2];
 #pragma unroll
@@ -267,8 +259,14 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
                     for (int j = 1; j <= R; ++j)
                         ly[r][v] = fma(FD<R>::b(j), yc[R + r + j][v] + yc[R + r - j][v], ly[r][v]);
         }
+        double pc[RPT][2];                              // P at the own points of plane z
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const double2 t = *reinterpret_cast<const double2*>(pst + (size_t)s * L::PWT + (r0 + r) * TX + 2 * tx);
+            pc[r][0] = t.x; pc[r][1] = t.y;
+        }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);          // this warp is done with plane z's slot
+        if (lane == 0) mbar_arrive(&empty[s]);          // this warp is done with stage s
         const int64_t o = zoff(z0 + i) + own;
         auto put = [&](double* p, double a, double b) {
             if (scs) __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
@@ -280,27 +278,13 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 const double lap = fma(A.sx2, lx[r][v], fma(A.sy2, ly[r][v], A.sz2 * lz[r][v]));
-                o1[v] = fma(A.c1, lap, pp[0][r][v]);                // combine<LF>(P, -, lap, c1)
+                o1[v] = fma(A.c1, lap, pc[r][v]);                   // combine<LF>(P, -, lap, c1)
                 o2[v] = fma(A.c2, o1[v], q[R][r][v]);               // combine<LF>(X, -, O1, c2)
             }
             put(A.O1 + o + (int64_t)r * nx, o1[0], o1[1]);
             put(A.O2 + o + (int64_t)r * nx, o2[0], o2[1]);
             if constexpr (KIND == HALF_FE)                          // u_1 = u_0 + h v_0
-                put(A.O3 + o + (int64_t)r * nx, fma(A.c1, pp[0][r][0], q[R][r][0]),
-                    fma(A.c1, pp[0][r][1], q[R][r][1]));
-        }
-        // advance the P prefetch (plane i + PF, clamped inside the chunk) and the queue
-#pragma unroll
-        for (int k = 0; k < PF - 1; ++k)
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) { pp[k][r][0] = pp[k + 1][r][0]; pp[k][r][1] = pp[k + 1][r][1]; }
-        {
-            const int zk = z0 + min(i + PF, niter - 1);
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                const double2 t = ldp(A.P + zoff(zk) + own + (int64_t)r * nx);
-                pp[PF - 1][r][0] = t.x; pp[PF - 1][r][1] = t.y;
-            }
+                put(A.O3 + o + (int64_t)r * nx, fma(A.c1, pc[r][0], q[R][r][0]), fma(A.c1, pc[r][1], q[R][r][1]));
         }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j)
