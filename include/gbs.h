@@ -285,9 +285,9 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        v_{n+2}, u_{n+3} from S_v, U -- the two share no value), 64 x 32 tiles,
  *                        one register queue per CTA (default 1; 0 = the coupled pair kernel;
  *                        peer pushes always use the coupled kernel)
- *   "half_fe"      1/0   the forward-Euler substep through the same kernel (default 1)
+ *   "half_fe"      1/0   the forward-Euler substep through the same kernel (default 0)
  *   "half_tall"    1/0   64 x 32 tiles for the half kernel when ny % 32 == 0 (default 1)
- *   "half_rpt"     2/4   rows per thread of the tall half kernel (16 or 8 consumer warps; default 2)
+ *   "half_rpt"     2/4   rows per thread of the tall half kernel (16 or 8 warps; default 4)
  *   "l2hint_half"  bits  half kernel: 1 centre boxes evict_last, 2 streaming loads of the
  *                        pointwise field, 4 halo boxes evict_first, 8 streaming stores (default 11)
  *   "fuse2d"       1/0   2-D acoustics: two substeps per pass as the chain-U / chain-P

@@ -179,8 +179,10 @@ struct gbs_ctx {
     bool use_half = true;             // leap-frog pairs as two single-stencil-field launches, FE
                                       // through the same kernel (gbs_wave3d_half.cuh)
     bool half_tall = true;            // 64 x 32 tiles when ny allows
-    int half_rpt = 2;                 // rows per thread of the tall half kernel (2 or 4)
-    bool half_fe = true;              // FE through the half kernel
+    int half_rpt = 4;                 // rows per thread of the tall half kernel (2 or 4; 4 measured
+                                      // 2% faster on C5: 5.96 vs 6.10 ms per half)
+    bool half_fe = false;             // FE through the half kernel (7.7 ms vs 7.5 for the FE step
+                                      // kernel on C5: off by default)
     int hint_half_opt = 11;           // half kernel L2 / streaming bits (HalfArgs::hint)
     bool loop_nccl = false;           // loopback halos through NCCL on a one-rank communicator
     // peer halo pushes (gbs_wave3d_tma.cuh PeerPush): option "peer" (loopback slabs) or
