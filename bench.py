@@ -356,7 +356,7 @@ def run_ours(a):
         # recorded by the library around every stencil launch on its stream
         # (time_kernels; launched without the graph, so region 1 alone gives the metric)
         gbs.gbs_set_option(st.ctx, "time_kernels", 1)
-        for cls in range(6):
+        for cls in range(8):
             gbs.gbs_kernel_time(st.ctx, cls, reset=True)
         barrier()
         t_ms = timed(a.steps)
@@ -364,7 +364,7 @@ def run_ours(a):
         gbs.gbs_sync(st.ctx)
         ms_instr = max_over_ranks(t_ms)
         del scratch
-        ktimes = {cls: gbs.gbs_kernel_time(st.ctx, cls) for cls in range(6)}
+        ktimes = {cls: gbs.gbs_kernel_time(st.ctx, cls) for cls in range(8)}
         gbs.gbs_set_option(st.ctx, "time_kernels", 0)
 
     S = info["substeps_per_macro"]
@@ -379,13 +379,18 @@ def run_ours(a):
             2: ("final substep + averaging + weighted accumulate", 24 * F),
             3: ("two leap-frog substeps in one pass", 48 * F),
             4: ("leap-frog + final substep in one pass", 48 * F),
-            5: ("whole-run cluster kernel", 24 * F * S * run_len)}
+            5: ("whole-run cluster kernel", 24 * F * S * run_len),
+            6: ("one single-stencil-field half of a two-substep pass", 24 * F),
+            7: ("unused", 0)}
     # bytes per point the kernel itself must read + write once (its own minimum HBM
     # traffic): the two-substep 3-D kernel moves S_u, U, S_v, P_v in and A_v, B, C_u out
     # (gbs_wave3d_pair.cuh) = 64 B instead of the metric's 2 x 24F = 96 B, and the FE
     # launch before it also writes u_2 (40 B); elsewhere it equals the metric's figure
-    fused3d = w.pde == "wave3d" and ktimes.get(3, (0, 0))[1] > 0
-    MOVED = {0: 24 * F, 1: 16 * F + (8 if fused3d else 0), 3: 64}
+    fused3d = w.pde == "wave3d" and (ktimes.get(3, (0, 0))[1] > 0 or ktimes.get(6, (0, 0))[1] > 0)
+    # half (class 6): reads X, P and writes O1, O2 = 32 B (its 24F = 48 B algorithmic figure: each of
+    # the pair's two substeps is completed by one of the two halves); LF + FIN pass: 32 B of levels
+    # + 16 B accumulator in, 16 B out (FIN0: no accumulator read; counted as FINACC)
+    MOVED = {0: 24 * F, 1: 16 * F + (8 if fused3d else 0), 3: 64, 4: 64, 6: 32}
     dom = max(ktimes, key=lambda c: ktimes[c][0])
     dom_ms, dom_n = ktimes[dom]
     avg = dom_ms / max(dom_n, 1)

@@ -565,7 +565,8 @@ def test_peer_halo_pushes_match_exchange(torch_cuda, cfg, n, slabs):
     w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8")
     y0, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "peer": 1})
-    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": 0})
+    # (peer pushes run the coupled pair kernel: compare launch counts with half = 0)
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts={"loopback": slabs, "overlap": 0, "half": 0})
     _, c1, _ = run_gpu(torch_cuda, w, counts, wd, H, 2)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[0], c1[0])
     # one stencil launch + one epoch signal per slab per substep launch, no exchange

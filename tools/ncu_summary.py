@@ -74,10 +74,11 @@ def full(path, traffic_cfg=None, cls=0):
             print(f"  {r[si][:28]:28s} {r[mi][:52]:52s} {r[vi]:>16s} {r[ui]}")
 
 
-def stalls(path, top=10):
+def stalls(path, top=10, skip=0):
     """Warp-stall sampling totals and the instructions with the most samples per reason
-    (source page, SASS view; needs --import-source / -lineinfo)."""
-    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+    (source page, SASS view; needs --import-source / -lineinfo) of the profiled launch `skip`."""
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass",
+                          "--launch-skip", str(skip), "--launch-count", "1"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
@@ -111,7 +112,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
     elif sys.argv[1] == "stalls":
-        stalls(sys.argv[2])
+        stalls(sys.argv[2], skip=int(sys.argv[sys.argv.index("--launch") + 1]) if "--launch" in sys.argv else 0)
     else:
         cfg = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
         cls = int(sys.argv[sys.argv.index("--class") + 1]) if "--class" in sys.argv else 0
