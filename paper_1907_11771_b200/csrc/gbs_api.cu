@@ -110,6 +110,8 @@ void gbs_destroy(gbs_ctx* c) {
     if (c->d_wh) cudaFree(c->d_wh);
     if (c->d_alpha) cudaFree(c->d_alpha);
     if (c->d_peer_flags) cudaFree(c->d_peer_flags);
+    if (c->d_stage) cudaFree(c->d_stage);
+    if (c->d_fence) cudaFree(c->d_fence);
     spectral_release(c);
     for (auto e : c->timer.ev) cudaEventDestroy(e);
     comm_release(c);
@@ -217,6 +219,16 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
         return GBS_OK;
     }
     if (k == "persistent") { c->use_persistent = value != 0; return GBS_OK; }
+    if (k == "fused_combine") {
+        // the final pass stores into the owners' staging slots of the other group members'
+        // contexts: needs groups > 1 with the members in this process (local transport)
+        if (value && (c->groups < 2 || !c->comm_group || !c->local_transport))
+            return fail(c, GBS_E_UNSUPPORTED, "fused_combine needs sequence groups whose contexts share this "
+                                              "process (GBS_TRANSPORT_LOCAL); NCCL contexts use ncclAllReduce");
+        c->fused_combine = value != 0;
+        drop_graphs();
+        return GBS_OK;
+    }
     if (k == "loopback") {
         if (value < 1) return fail(c, GBS_E_INVAL, "loopback must be >= 1");
         if (c->world > 1) return fail(c, GBS_E_UNSUPPORTED, "loopback needs a single-GPU context");

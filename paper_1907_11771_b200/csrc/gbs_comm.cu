@@ -80,6 +80,11 @@ struct NcclComm final : Comm {
         NC(c, nccl::api().AllGather(src, dst, n, nccl::ncclFloat64, h, st));
         return GBS_OK;
     }
+    int fence(gbs_ctx* c, cudaStream_t st) override {
+        if (!c->d_fence) CU(c, cudaMalloc(&c->d_fence, sizeof(double)));
+        NC(c, nccl::api().AllReduce(c->d_fence, c->d_fence, 1, nccl::ncclFloat64, nccl::ncclSum, h, st));
+        return GBS_OK;
+    }
     int split(gbs_ctx* c, int color, int key, Comm** out) override {
         nccl::comm_t s = nullptr;
         int r = nccl::api().CommSplit(h, color, key, &s, nullptr);
@@ -109,6 +114,32 @@ __global__ void local_sum_kernel(SumPtrs P, int n, int64_t e0, int64_t e1) {
     }
 }
 
+}  // namespace
+
+// the fused combine's owner step: out_j[e] = sum_i in_i[e] (member order) for every member j
+__global__ void owner_combine_kernel(SumPtrs in, SumPtrs out, int n, int64_t count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride) {
+        double s = in.p[0][e];
+        for (int i = 1; i < n; ++i) s += in.p[i][e];
+        for (int j = 0; j < n; ++j) out.p[j][e] = s;
+    }
+}
+
+int owner_combine(gbs_ctx* c, double* const* in, double* const* out, int n, int64_t count, cudaStream_t st) {
+    if (n > kMaxMembers) return fail(c, GBS_E_UNSUPPORTED, "fused combine: > %d groups", kMaxMembers);
+    if (count <= 0) return GBS_OK;
+    SumPtrs I{}, O{};
+    for (int i = 0; i < n; ++i) { I.p[i] = in[i]; O.p[i] = out[i]; }
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)c->sms * 8);
+    owner_combine_kernel<<<(unsigned)blocks, 256, 0, st>>>(I, O, n, count);
+    CU(c, cudaGetLastError());
+    c->launches++;
+    return GBS_OK;
+}
+
+namespace {
+
 struct Posted {
     int kind;            // 0 send, 1 recv
     int peer;
@@ -128,12 +159,14 @@ struct Shared {
     std::vector<std::vector<Posted>> posted;  // per member (p2p groups)
     std::vector<std::vector<double*>> bufs;   // per member (allreduce / allgather arguments)
     std::vector<std::vector<size_t>> counts;
+    std::vector<gbs_ctx*> ctx;                // per member (local transport: same process)
     std::vector<std::pair<int, int>> split_in;                          // (color, key) per member
     std::vector<std::pair<std::shared_ptr<Shared>, int>> split_out;    // (communicator, rank)
     bool broken = false;
 
     explicit Shared(int n_, int dev) : n(n_), device(dev), ready(n_, nullptr), done(n_, nullptr),
-                                       posted(n_), bufs(n_), counts(n_), split_in(n_), split_out(n_) {}
+                                       posted(n_), bufs(n_), counts(n_), ctx(n_, nullptr), split_in(n_),
+                                       split_out(n_) {}
     ~Shared() {
         for (auto e : ready) if (e) cudaEventDestroy(e);
         for (auto e : done) if (e) cudaEventDestroy(e);
@@ -288,6 +321,18 @@ struct LocalComm final : Comm {
             if (j != rank) CU(c, cudaStreamWaitEvent(st, S->done[j], 0));
         return GBS_OK;
     }
+    int fence(gbs_ctx* c, cudaStream_t st) override {
+        int rc;
+        if ((rc = ev_init(c))) return rc;
+        CU(c, cudaEventRecord(S->ready[rank], st));
+        if ((rc = bar(c))) return rc;
+        for (int j = 0; j < size; ++j)
+            if (j != rank) CU(c, cudaStreamWaitEvent(st, S->ready[j], 0));
+        // nobody records READY again before every member has enqueued its waits
+        return bar(c);
+    }
+    gbs_ctx* member_ctx(int i) override { return (i >= 0 && i < size) ? S->ctx[i] : nullptr; }
+    void register_ctx(gbs_ctx* c) override { S->ctx[rank] = c; }
     int split(gbs_ctx* c, int color, int key, Comm** out) override {
         int rc;
         S->split_in[rank] = {color, key};
@@ -346,6 +391,7 @@ int comm_init(gbs_ctx* c, const gbs_dist* d) {
     g->rank = c->my_group; g->size = c->groups;
     c->comm_slab = s;
     c->comm_group = g;
+    c->comm_group->register_ctx(c);
     return GBS_OK;
 }
 

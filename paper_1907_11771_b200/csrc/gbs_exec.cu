@@ -252,6 +252,67 @@ static int ac2d_pair_step(gbs_ctx* c, int cls, int P, int S, int Aout, int Bout,
     return GBS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fused combine across sequence groups (option "fused_combine"; PAPER.md:109-115,
+// 398-400).  The slab's planes are split into g owner ranges, range j owned by group j.  The
+// final pass of this group's last sequence is launched once per range j and stores its
+// w-scaled partial sum straight into owner j's staging slot for this group (a store into the
+// other context's memory: peer memory across GPUs, the same device here); after a fence every
+// owner sums the g slots of its range in member order and stores the sum into every member's
+// accumulator; a second fence and the accumulator is the next Y everywhere.  Same sums in the
+// same order as the local transport's all-reduce: bit-identical to it.
+// ---------------------------------------------------------------------------
+static void owner_range(int64_t nz, int g, int j, int64_t* lo, int64_t* hi) {
+    *lo = nz * j / g;
+    *hi = nz * (j + 1) / g;
+}
+
+static int fused_final_pass(gbs_ctx* c, const PairOperands& fin) {
+    const int g = c->groups, me = c->my_group, F = c->F;
+    Slab& s = c->slab[0];
+    const int64_t P = c->plane;
+    int rc;
+    if (!c->d_stage) {
+        int64_t lo, hi;
+        owner_range(s.nz, g, me, &lo, &hi);
+        c->stage_doubles = (int64_t)g * F * (hi - lo) * P;
+        CU(c, cudaMalloc(&c->d_stage, sizeof(double) * (size_t)std::max<int64_t>(c->stage_doubles, 1)));
+    }
+    // the halos of the stencil operands, then the pass per owner range (no overlap split)
+    if (c->ghost > 0 && c->slabs > 1) {
+        if ((rc = exchange_halo(c, fin.Su.b, 1u << fin.Su.f))) return rc;
+        if ((rc = exchange_halo(c, fin.U.b, 1u << fin.U.f))) return rc;
+    }
+    // every member has allocated its staging buffer and finished reading its previous ones
+    if ((rc = c->comm_group->fence(c, c->stream))) return rc;
+    for (int j = 0; j < g; ++j) {
+        gbs_ctx* o = c->comm_group->member_ctx(j);
+        if (!o || !o->d_stage) return fail(c, GBS_E_STATE, "fused combine: member %d has no staging buffer", j);
+        int64_t lo, hi;
+        owner_range(s.nz, g, j, &lo, &hi);
+        if (hi <= lo) continue;
+        PairOperands op = fin;
+        // plane z of this slab lands at slot (me, f) of owner j, offset by its first plane
+        op.out_u = o->d_stage + ((int64_t)(me * F + 0) * (hi - lo) - lo) * P;
+        op.out_v = o->d_stage + ((int64_t)(me * F + 1) * (hi - lo) - lo) * P;
+        if ((rc = launch_pair(c, s, op, lo, hi, 0))) return rc;
+    }
+    if ((rc = c->comm_group->fence(c, c->stream))) return rc;
+    int64_t lo, hi;
+    owner_range(s.nz, g, me, &lo, &hi);
+    const int ACC = fin.Bu.b;
+    for (int f = 0; f < F; ++f) {
+        std::vector<double*> in(g), out(g);
+        for (int i = 0; i < g; ++i) {
+            in[i] = c->d_stage + (int64_t)(i * F + f) * (hi - lo) * P;
+            gbs_ctx* o = c->comm_group->member_ctx(i);
+            out[i] = field_ptr(o, o->slab[0], ACC, f) + lo * P;
+        }
+        if ((rc = owner_combine(c, in.data(), out.data(), g, (hi - lo) * P, c->stream))) return rc;
+    }
+    return c->comm_group->fence(c, c->stream);
+}
+
 static bool fused_path(const gbs_ctx* c) {
     if (!(c->use_fuse && c->use_bulk && c->nbuf == 6)) return false;
     for (const auto& s : c->slab)
@@ -282,6 +343,7 @@ static int enqueue_macro(gbs_ctx* c, double H) {
     const int64_t l0 = c->launches;
     int rc;
     bool first = true;
+    bool combined = false;            // the fused combine already summed the groups
     const bool fused = fused_path(c) && c->pde == GBS_WAVE3D;
     bool fused2d = fused_path(c) && c->use_fuse2d && c->pde == GBS_ACOUSTIC2D;
     for (const auto& s : c->slab)                  // the chain kernels work in whole 32-row bands
@@ -346,7 +408,12 @@ static int enqueue_macro(gbs_ctx* c, double H) {
                     PairOperands fin{Pv, Su, Sv, U, Slot{ACC, 0}, Slot{ACC, 0}, Slot{ACC, 1}, Slot{ACC, 0},
                                      first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, 2.0 * h, h,
                                      0.5 * c->wk_all[k], last};
-                    if ((rc = pair_step(c, 4, fin))) return rc;
+                    if (last && c->fused_combine && c->groups > 1) {
+                        if ((rc = fused_final_pass(c, fin))) return rc;
+                        combined = true;
+                    } else if ((rc = pair_step(c, 4, fin))) {
+                        return rc;
+                    }
                 }
             }
             first = false;
@@ -364,7 +431,7 @@ static int enqueue_macro(gbs_ctx* c, double H) {
         if ((rc = step(c, 2, fin))) return rc;
         first = false;
     }
-    if (c->groups > 1) {
+    if (c->groups > 1 && !combined) {
         // Y <- sum over the sequence groups of their w-scaled partial sums
         Slab& s = c->slab[0];
         double* p[3];

@@ -88,6 +88,12 @@ struct Comm {
     // dst[j*n .. (j+1)*n) <- member j's src
     virtual int allgather(gbs_ctx* c, const double* src, double* dst, size_t n, cudaStream_t st) = 0;
     virtual int split(gbs_ctx* c, int color, int key, Comm** out) = 0;
+    // device-side barrier of the members on stream st: work enqueued after it runs after every
+    // member's work enqueued before it (local: events + host barrier; NCCL: a 1-value all-reduce)
+    virtual int fence(gbs_ctx* c, cudaStream_t st) = 0;
+    // member i's context when the members share this process (local transport), else nullptr
+    virtual gbs_ctx* member_ctx(int) { return nullptr; }
+    virtual void register_ctx(gbs_ctx*) {}
 };
 int comm_init(gbs_ctx* c, const gbs_dist* d);   // world, slab and group communicators
 int comm_nccl_self(gbs_ctx* c, Comm** out);      // one-rank NCCL communicator (loopback_nccl)
@@ -133,6 +139,14 @@ struct gbs_ctx {
     Comm* comm_slab = nullptr;        // the slabs of this rank's sequence group (halo exchange, gather)
     Comm* comm_group = nullptr;       // the groups holding this rank's slab (combine)
     bool local_transport = false;     // ranks are contexts of this process (gbs_local_hub_create)
+    // fused combine across sequence groups (option "fused_combine"): the last
+    // final pass of each group stores its w-scaled partial of owner j's plane range straight
+    // into j's staging slot; each owner sums its range in member order and stores the sum into
+    // every member's accumulator (reduce-scatter + all-gather without a collective call)
+    bool fused_combine = false;
+    double* d_stage = nullptr;        // [source group][field][planes of my range][plane]
+    int64_t stage_doubles = 0;
+    double* d_fence = nullptr;        // NCCL fence operand (Comm::fence)
     // memory
     std::vector<Slab> slab;
     int64_t ghost = 0;                // ghost planes per side (R when slabbed)
@@ -253,6 +267,10 @@ struct PairOperands {
     int modeB;
     double cfA, cfB, wh;
     bool flag;
+    // FIN modes: store the result here instead of the accumulator buffer (plane z at
+    // out_u + z * plane; the accumulator is still read from Bu.b) -- the fused combine
+    double* out_u = nullptr;
+    double* out_v = nullptr;
 };
 
 // One single-stencil-field 3-D launch (gbs_wave3d_half.cuh): O1 = P + c1 lap(X),
@@ -295,6 +313,8 @@ constexpr int64_t kPeerFlagBytes = 256;    // workspace tail: this rank's two fl
 int spectral_setup(gbs_ctx* c);       // cuFFT plans + buffers (order 0); idempotent
 void spectral_release(gbs_ctx* c);
 int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);
+// ---- gbs_comm.cu
+int owner_combine(gbs_ctx* c, double* const* in, double* const* out, int n, int64_t count, cudaStream_t st);
 // ---- gbs_exec.cu
 int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev);
 int harvest_timer(gbs_ctx* c);

@@ -487,7 +487,8 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
         a.Cu = field_ptr(c, s, op.Cu.b, op.Cu.f);
     } else {
         a.Av = a.Cu = nullptr;
-        a.Bu = field_ptr(c, s, op.Bu.b, 0); a.Bv = field_ptr(c, s, op.Bu.b, 1);
+        a.Bu = op.out_u ? op.out_u : field_ptr(c, s, op.Bu.b, 0);
+        a.Bv = op.out_v ? op.out_v : field_ptr(c, s, op.Bu.b, 1);
     }
     a.Su = field_ptr(c, s, op.Su.b, op.Su.f);
     a.U = field_ptr(c, s, op.U.b, op.U.f);

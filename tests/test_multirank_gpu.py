@@ -165,3 +165,32 @@ def test_planner_choice_runs(torch_cuda):
     counts, wd, H = scheme_for(w, "nonzero8", "c5")
     plan = gbs.gbs_plan(w.pde, w.n, w.order, counts, 8, 0, 0)
     check(torch_cuda, "c5", (128, 16, 64), 1, 8, plan["groups"])
+
+
+# fused combine: the final pass stores into the owners' staging slots, owners sum
+# their plane range in member order and store into every member -- bit-identical to the
+# transport's all-reduce (same sums, same order) and the oracle's result within the bar
+@pytest.mark.parametrize("cfg,n,world,groups", [("c4", (64, 32, 48), 2, 2), ("c4", (64, 32, 48), 4, 2),
+                                                ("c5", (128, 16, 96), 8, 4), ("c5", (64, 16, 64), 4, 4),
+                                                ("c4", (64, 32, 24), 8, 8)])
+def test_fused_combine_equals_allreduce(torch_cuda, cfg, n, world, groups):
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8", cfg)
+    y0, a, ia = run_ranks(torch_cuda, w, counts, wd, H, 2, world, groups, {"fused_combine": 1})
+    _, b, ib = run_ranks(torch_cuda, w, counts, wd, H, 2, world, groups, {"fused_combine": 0})
+    for r in range(world):
+        assert np.array_equal(a[r], b[r])
+    ref = C.advance(w.pde, w.order, y0, counts, wd, H, 2)
+    rel, mrms, mmax = errors(a[0], ref)
+    record_parity(f"multirank fused combine {cfg} {n} world={world} groups={groups}", rel, mrms, mmax)
+    assert rel <= TOL and mmax <= TOL_ELEM
+
+
+def test_fused_combine_rejected_without_local_groups(torch_cuda):
+    from paper_1907_11771_b200 import gbs
+    w = reduced("c4", (64, 32, 24), macro_steps=1, weights="nonzero8")
+    counts, wd, _ = scheme_for(w, "nonzero8", "c4")
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:       # one context, no groups
+        with pytest.raises(gbs.GbsError) as e:
+            gbs.gbs_set_option(st.ctx, "fused_combine", 1)
+        assert e.value.code == gbs.GBS_E_UNSUPPORTED
