@@ -244,6 +244,26 @@ GBS_API int gbs_bind_workspace(gbs_ctx* ctx, void* device_ptr, int64_t bytes);
  * Not yet run on more than one GPU. */
 GBS_API int gbs_bind_peers(gbs_ctx* ctx, void* lower_workspace, void* upper_workspace);
 
+/* Fused combine across sequence groups (the groups'
+ * w-scaled partial sums are added).  The slab's planes are split into g owner ranges (range j =
+ * planes [nz j / g, nz (j+1) / g) owned by group j).  The final pass of each group's last
+ * sequence (3-D two-substep path) stores its partial sum of range j straight into owner j's
+ * staging buffer (peer memory), each owner sums the g slots of its range in member order and
+ * stores the sum into every member's accumulator -- a reduce-scatter and an all-gather with no
+ * collective call; a device-side fence between the phases (local transport: events and host
+ * barriers; NCCL: a one-value all-reduce on the group communicator).  Bit-identical to the
+ * local transport's all-reduce (same sums in the same order).
+ *   option "fused_combine" 1   the local transport (members are contexts of this process)
+ *   gbs_stage_bytes            bytes of one member's staging buffer (g F max-range planes)
+ *   gbs_bind_group_peers       member_workspaces[j] / member_stages[j]: group member j's bound
+ *                              workspace (gbs_bind_workspace; same layout on every member) and
+ *                              staging buffer, mapped into this process (e.g. torch symmetric
+ *                              memory); member_workspaces[my_group] must be this context's own.
+ *                              Turns the fused combine on; n = 0 turns it off.  GBS_E_STATE
+ *                              without a workspace.  Not yet run across GPUs. */
+GBS_API int gbs_stage_bytes(const gbs_ctx* ctx, int64_t* bytes);
+GBS_API int gbs_bind_group_peers(gbs_ctx* ctx, void* const* member_workspaces, void* const* member_stages, int n);
+
 /* Asynchronous slab IO (same layout and count as gbs_write_slab / gbs_read_slab; on one
  * GPU the slab is the whole grid).  The copies run on the context's own copy streams and
  * overlap the macro steps queued on the context stream:
@@ -306,6 +326,8 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        stores (default 11; results do not depend on it)
  *   "l2hint_step"  bits  the same for the single-substep 3-D TMA kernel (1 = tile boxes
  *                        evict_last; default 0)
+ *   "fused_combine" 1/0  sequence groups of the local transport: the fused combine above
+ *                        (default 0: Comm all-reduce)
  *   "peer"         1/0   loopback slabs of a 3-D TMA grid: face planes pushed into the
  *                        neighbouring slabs' ghost planes by the producing kernels, ordered
  *                        by epoch flags (gbs_bind_peers), no halo exchange (default 0)

@@ -222,9 +222,9 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "fused_combine") {
         // the final pass stores into the owners' staging slots of the other group members'
         // contexts: needs groups > 1 with the members in this process (local transport)
-        if (value && (c->groups < 2 || !c->comm_group || !c->local_transport))
+        if (value && (c->groups < 2 || !c->comm_group || (!c->local_transport && c->grp_ws.empty())))
             return fail(c, GBS_E_UNSUPPORTED, "fused_combine needs sequence groups whose contexts share this "
-                                              "process (GBS_TRANSPORT_LOCAL); NCCL contexts use ncclAllReduce");
+                                              "process (GBS_TRANSPORT_LOCAL) or gbs_bind_group_peers");
         c->fused_combine = value != 0;
         drop_graphs();
         return GBS_OK;
@@ -275,6 +275,9 @@ int gbs_bind_workspace(gbs_ctx* c, void* device_ptr, int64_t bytes) {
     c->have_state = false;              // the state must be written again
     c->peer_on = false;                 // peers are bound to a workspace
     c->peer_base[0] = c->peer_base[1] = nullptr;
+    if (!c->grp_ws.empty()) c->fused_combine = false;   // so are the group members'
+    c->grp_ws.clear();
+    c->grp_stage.clear();
     if (device_ptr) {
         CU(c, cudaMemset(static_cast<char*>(device_ptr) + state_bytes(c), 0, kPeerFlagBytes));
         c->peer_flags_fresh = true;
@@ -307,6 +310,39 @@ int gbs_bind_peers(gbs_ctx* c, void* lower_workspace, void* upper_workspace) {
     c->peer_flags_fresh = false;
     c->peer_on = true;
     c->peer_ghosts_valid = false;
+    return GBS_OK;
+}
+
+int gbs_stage_bytes(const gbs_ctx* c, int64_t* bytes) {
+    if (!c || !bytes) return fail(const_cast<gbs_ctx*>(c), GBS_E_INVAL, "ctx or bytes is NULL");
+    *bytes = c->groups > 1 ? stage_bytes_of(c) : 0;
+    return GBS_OK;
+}
+
+int gbs_bind_group_peers(gbs_ctx* c, void* const* member_workspaces, void* const* member_stages, int n) {
+    if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    if (n == 0 || !member_workspaces || !member_stages) {
+        c->grp_ws.clear();
+        c->grp_stage.clear();
+        c->fused_combine = false;
+        return GBS_OK;
+    }
+    if (c->groups < 2 || n != c->groups)
+        return fail(c, GBS_E_INVAL, "n=%d must equal the sequence groups (%d, >= 2)", n, c->groups);
+    if (!c->ws_ptr) return fail(c, GBS_E_STATE, "gbs_bind_group_peers needs a bound workspace (gbs_bind_workspace)");
+    if (member_workspaces[c->my_group] != c->ws_ptr)
+        return fail(c, GBS_E_INVAL, "member_workspaces[my_group] is not this context's workspace");
+    for (int j = 0; j < n; ++j)
+        if (!member_workspaces[j] || !member_stages[j]) return fail(c, GBS_E_INVAL, "member %d pointer is NULL", j);
+    CU(c, cudaSetDevice(c->device));
+    CU(c, cudaStreamSynchronize(c->stream));
+    c->grp_ws.assign(n, nullptr);
+    c->grp_stage.assign(n, nullptr);
+    for (int j = 0; j < n; ++j) {
+        c->grp_ws[j] = static_cast<char*>(member_workspaces[j]);
+        c->grp_stage[j] = static_cast<char*>(member_stages[j]);
+    }
+    c->fused_combine = true;
     return GBS_OK;
 }
 

@@ -267,17 +267,41 @@ static void owner_range(int64_t nz, int g, int j, int64_t* lo, int64_t* hi) {
     *hi = nz * (j + 1) / g;
 }
 
+int64_t stage_bytes_of(const gbs_ctx* c) {
+    int64_t mx = 0;
+    const int64_t nz = c->nslow / std::max(1, c->slabs);
+    for (int j = 0; j < c->groups; ++j) {
+        int64_t lo, hi;
+        owner_range(nz, c->groups, j, &lo, &hi);
+        mx = std::max(mx, hi - lo);
+    }
+    return (int64_t)sizeof(double) * c->groups * c->F * mx * c->plane;
+}
+
+// member j's staging buffer and the base of its field f of buffer b (same layout on every member)
+static double* member_stage(gbs_ctx* c, int j) {
+    if (!c->grp_stage.empty()) return reinterpret_cast<double*>(c->grp_stage[j]);
+    gbs_ctx* o = c->comm_group->member_ctx(j);
+    return o ? o->d_stage : nullptr;
+}
+static double* member_field(gbs_ctx* c, int j, int b, int f) {
+    double* mine = field_ptr(c, c->slab[0], b, f);
+    if (!c->grp_ws.empty())
+        return reinterpret_cast<double*>(c->grp_ws[j] + (reinterpret_cast<char*>(mine) - static_cast<char*>(c->ws_ptr)));
+    gbs_ctx* o = c->comm_group->member_ctx(j);
+    return o ? field_ptr(o, o->slab[0], b, f) : nullptr;
+}
+
 static int fused_final_pass(gbs_ctx* c, const PairOperands& fin) {
     const int g = c->groups, me = c->my_group, F = c->F;
     Slab& s = c->slab[0];
     const int64_t P = c->plane;
     int rc;
-    if (!c->d_stage) {
-        int64_t lo, hi;
-        owner_range(s.nz, g, me, &lo, &hi);
-        c->stage_doubles = (int64_t)g * F * (hi - lo) * P;
+    if (c->grp_stage.empty() && !c->d_stage) {
+        c->stage_doubles = stage_bytes_of(c) / (int64_t)sizeof(double);
         CU(c, cudaMalloc(&c->d_stage, sizeof(double) * (size_t)std::max<int64_t>(c->stage_doubles, 1)));
     }
+    double* my_stage = member_stage(c, me);
     // the halos of the stencil operands, then the pass per owner range (no overlap split)
     if (c->ghost > 0 && c->slabs > 1) {
         if ((rc = exchange_halo(c, fin.Su.b, 1u << fin.Su.f))) return rc;
@@ -286,15 +310,15 @@ static int fused_final_pass(gbs_ctx* c, const PairOperands& fin) {
     // every member has allocated its staging buffer and finished reading its previous ones
     if ((rc = c->comm_group->fence(c, c->stream))) return rc;
     for (int j = 0; j < g; ++j) {
-        gbs_ctx* o = c->comm_group->member_ctx(j);
-        if (!o || !o->d_stage) return fail(c, GBS_E_STATE, "fused combine: member %d has no staging buffer", j);
+        double* st = member_stage(c, j);
+        if (!st) return fail(c, GBS_E_STATE, "fused combine: member %d has no staging buffer", j);
         int64_t lo, hi;
         owner_range(s.nz, g, j, &lo, &hi);
         if (hi <= lo) continue;
         PairOperands op = fin;
         // plane z of this slab lands at slot (me, f) of owner j, offset by its first plane
-        op.out_u = o->d_stage + ((int64_t)(me * F + 0) * (hi - lo) - lo) * P;
-        op.out_v = o->d_stage + ((int64_t)(me * F + 1) * (hi - lo) - lo) * P;
+        op.out_u = st + ((int64_t)(me * F + 0) * (hi - lo) - lo) * P;
+        op.out_v = st + ((int64_t)(me * F + 1) * (hi - lo) - lo) * P;
         if ((rc = launch_pair(c, s, op, lo, hi, 0))) return rc;
     }
     if ((rc = c->comm_group->fence(c, c->stream))) return rc;
@@ -304,9 +328,10 @@ static int fused_final_pass(gbs_ctx* c, const PairOperands& fin) {
     for (int f = 0; f < F; ++f) {
         std::vector<double*> in(g), out(g);
         for (int i = 0; i < g; ++i) {
-            in[i] = c->d_stage + (int64_t)(i * F + f) * (hi - lo) * P;
-            gbs_ctx* o = c->comm_group->member_ctx(i);
-            out[i] = field_ptr(o, o->slab[0], ACC, f) + lo * P;
+            in[i] = my_stage + (int64_t)(i * F + f) * (hi - lo) * P;
+            double* acc = member_field(c, i, ACC, f);
+            if (!acc) return fail(c, GBS_E_STATE, "fused combine: member %d's accumulator unknown", i);
+            out[i] = acc + lo * P;
         }
         if ((rc = owner_combine(c, in.data(), out.data(), g, (hi - lo) * P, c->stream))) return rc;
     }

@@ -147,6 +147,9 @@ struct gbs_ctx {
     double* d_stage = nullptr;        // [source group][field][planes of my range][plane]
     int64_t stage_doubles = 0;
     double* d_fence = nullptr;        // NCCL fence operand (Comm::fence)
+    // gbs_bind_group_peers: every group member's workspace and staging buffer mapped into this
+    // process (peer memory across GPUs); empty = the members' contexts (local transport)
+    std::vector<char*> grp_ws, grp_stage;
     // memory
     std::vector<Slab> slab;
     int64_t ghost = 0;                // ghost planes per side (R when slabbed)
@@ -316,6 +319,7 @@ int launch_cluster_run(gbs_ctx* c, int64_t macro_steps, double H);
 // ---- gbs_comm.cu
 int owner_combine(gbs_ctx* c, double* const* in, double* const* out, int n, int64_t count, cudaStream_t st);
 // ---- gbs_exec.cu
+int64_t stage_bytes_of(const gbs_ctx* c);     // staging buffer of the fused combine
 int timed_begin(gbs_ctx* c, int cls, cudaEvent_t* end_ev);
 int harvest_timer(gbs_ctx* c);
 // ---- gbs_io.cu

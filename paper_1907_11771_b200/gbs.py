@@ -31,7 +31,7 @@ EXPORTS = ["gbs_create", "gbs_write_state", "gbs_advance", "gbs_read_state", "gb
            "gbs_destroy", "gbs_nccl_unique_id", "gbs_query", "gbs_plan", "gbs_halo_schedule",
            "gbs_set_option",
            "gbs_kernel_time", "gbs_strerror", "gbs_last_error", "gbs_local_hub_create",
-           "gbs_local_hub_destroy"]
+           "gbs_local_hub_destroy", "gbs_stage_bytes", "gbs_bind_group_peers"]
 GBS_TRANSPORT_NCCL, GBS_TRANSPORT_LOCAL = 0, 1
 
 
@@ -130,6 +130,8 @@ def load(build_if_missing: bool = False):
                                     ctypes.POINTER(gbs_halo_op), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     L.gbs_set_option.argtypes = [vp, ctypes.c_char_p, i64]
     L.gbs_kernel_time.argtypes = [vp, ctypes.c_int, dp, ctypes.POINTER(i64), ctypes.c_int]
+    L.gbs_stage_bytes.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+    L.gbs_bind_group_peers.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.c_int]
     L.gbs_local_hub_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.gbs_local_hub_destroy.argtypes = [vp]
     L.gbs_local_hub_destroy.restype = None
@@ -316,6 +318,24 @@ def gbs_bind_peers(ctx, lower_ptr, upper_ptr) -> None:
     lo = ctypes.c_void_p(int(lower_ptr)) if lower_ptr else None
     hi = ctypes.c_void_p(int(upper_ptr)) if upper_ptr else None
     _check(load().gbs_bind_peers(ctx, lo, hi), ctx)
+
+
+def gbs_stage_bytes(ctx) -> int:
+    b = ctypes.c_int64(0)
+    _check(load().gbs_stage_bytes(ctx, ctypes.byref(b)), ctx)
+    return b.value
+
+
+def gbs_bind_group_peers(ctx, member_workspaces, member_stages) -> None:
+    """Fused combine across sequence groups: every group member's workspace and staging buffer
+    as device addresses mapped into this process (ints, group order), or [] to turn it off."""
+    n = len(member_workspaces)
+    if n == 0:
+        _check(load().gbs_bind_group_peers(ctx, None, None, 0), ctx)
+        return
+    W = (ctypes.c_void_p * n)(*[int(p) for p in member_workspaces])
+    S = (ctypes.c_void_p * n)(*[int(p) for p in member_stages])
+    _check(load().gbs_bind_group_peers(ctx, W, S, n), ctx)
 
 
 def gbs_bind_workspace(ctx, ws) -> None:

@@ -172,7 +172,7 @@ def test_planner_choice_runs(torch_cuda):
 # transport's all-reduce (same sums, same order) and the oracle's result within the bar
 @pytest.mark.parametrize("cfg,n,world,groups", [("c4", (64, 32, 48), 2, 2), ("c4", (64, 32, 48), 4, 2),
                                                 ("c5", (128, 16, 96), 8, 4), ("c5", (64, 16, 64), 4, 4),
-                                                ("c4", (64, 32, 24), 8, 8)])
+                                                ("c5", (64, 16, 64), 8, 8)])
 def test_fused_combine_equals_allreduce(torch_cuda, cfg, n, world, groups):
     w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8", cfg)
@@ -194,3 +194,43 @@ def test_fused_combine_rejected_without_local_groups(torch_cuda):
         with pytest.raises(gbs.GbsError) as e:
             gbs.gbs_set_option(st.ctx, "fused_combine", 1)
         assert e.value.code == gbs.GBS_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("world,groups", [(2, 2), (4, 2), (8, 4)])
+def test_fused_combine_through_bound_peer_buffers(torch_cuda, world, groups):
+    """The multi-GPU form of the fused combine: each rank binds a torch workspace and a staging
+    tensor, and every group member's pair of addresses (peer memory across GPUs; the same device
+    here) through gbs_bind_group_peers.  Bit-identical to the all-reduce."""
+    import threading
+    from paper_1907_11771_b200 import gbs
+    w = reduced("c5", (64, 16, 64), macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8", "c5")
+    y0 = make_ic(w)
+    slabs = world // groups
+    ptrs = [None] * world
+    bar = threading.Barrier(world)
+
+    def body(dist):
+        torch = torch_cuda
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        r = dist["rank"]
+        with gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist, stream=s.cuda_stream,
+                         torch_memory=True) as st:
+            stage = torch.empty(max(gbs.gbs_stage_bytes(st.ctx), 1), dtype=torch.uint8, device="cuda")
+            ptrs[r] = (st.workspace.data_ptr(), stage.data_ptr())
+            bar.wait()
+            me = st.info()
+            members = [j * slabs + me["my_slab"] for j in range(groups)]
+            gbs.gbs_bind_group_peers(st.ctx, [ptrs[m][0] for m in members], [ptrs[m][1] for m in members])
+            st.write(y0)
+            st.advance(2, H)
+            out = np.empty_like(y0)
+            st.read(out)
+            bar.wait()                     # every member done before any staging tensor is freed
+            return out
+
+    a = gbs.run_local_ranks(world, body, groups=groups)
+    _, b, _ = run_ranks(torch_cuda, w, counts, wd, H, 2, world, groups, {"fused_combine": 0})
+    for r in range(world):
+        assert np.array_equal(a[r], b[r])
