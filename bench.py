@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--peers", action="store_true",
                     help="N > 1: halo planes pushed by the stencil kernels into the neighbours' "
                          "ghost planes through torch symmetric memory (gbs_bind_peers) instead of NCCL")
+    ap.add_argument("--fused-combine", action="store_true",
+                    help="N > 1 with sequence groups: the final pass stores into the owners' staging "
+                         "buffers through torch symmetric memory (gbs_bind_group_peers) instead of "
+                         "ncclAllReduce")
     ap.add_argument("--repeats", type=int, default=5,
                     help="extra K-step timed regions after the metric's (median / best reported "
                          "under 'repeats'; 'value' stays the first region)")
@@ -290,7 +294,8 @@ def run_ours(a):
         # the state buffers live in a torch tensor (gbs_bind_workspace): PyTorch owns device memory
         opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
         st = gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist_desc, stream=stream.cuda_stream,
-                         torch_memory=True, peers=a.peers and world > 1, **opts)
+                         torch_memory=True, peers=a.peers and world > 1,
+                         group_peers=a.fused_combine and world > 1, **opts)
         y0_dev = torch.from_numpy(y0).to("cuda", non_blocking=False)
         st.write_slab(y0_dev)
         gbs.gbs_sync(st.ctx)
@@ -480,6 +485,9 @@ def run_ours(a):
                                   "%.0f MiB < 2 x L2" % (6 * y0.nbytes / 2 ** 20) if flush else
                                   "inputs larger than L2 (each state buffer %.2f GiB)" % (y0.nbytes / 2 ** 30)),
                            "plan": {"groups": info["groups"], "slabs": info["slabs"]},
+                           "combine": ("none (one group)" if info["groups"] == 1 else
+                                       "fused: owner ranges through symmetric memory" if a.fused_combine
+                                       else "ncclAllReduce"),
                            "halo": ("peer pushes (symmetric memory)" if a.peers and world > 1 else
                                     "NCCL send/recv overlapped with the interior" if info["slabs"] > 1 else "none"),
                            "hbm_roofline_fraction_of_step": round(

@@ -397,24 +397,46 @@ class Stepper:
     """RAII convenience around one context (still only marshalling)."""
 
     def __init__(self, pde, n, stencil_order, n_k, w_k, dist=None, stream=None, torch_memory=False,
-                 peers=False, **opts):
+                 peers=False, group_peers=False, **opts):
         self.pde = pde
         self.ctx = gbs_create(pde, n, stencil_order, n_k, w_k, dist, stream)
         for k, v in opts.items():
             gbs_set_option(self.ctx, k, v)
         self.workspace = None
         self.symm = None
-        if torch_memory or peers:
+        self.stage = None
+        multi = bool(dist) and dist.get("world", 1) > 1 and dist.get("transport", 0) == GBS_TRANSPORT_NCCL
+        if torch_memory or peers or group_peers:
             # the state buffers live in a torch tensor (PyTorch's allocator owns the memory)
             import torch
             nbytes = max(gbs_workspace_bytes(self.ctx), 1)
-            if peers and dist and dist.get("world", 1) > 1:
-                self.workspace = self._peer_workspace(pde, n, stencil_order, n_k, dist, nbytes)
+            if (peers or group_peers) and multi:
+                self.workspace = self._peer_workspace(pde, n, stencil_order, n_k, dist, nbytes, halos=peers)
+                if group_peers:
+                    self._group_peers(pde, n, stencil_order, n_k, dist)
             else:
                 self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
                 gbs_bind_workspace(self.ctx, self.workspace)
 
-    def _peer_workspace(self, pde, n, stencil_order, n_k, dist, nbytes):
+    def _group_peers(self, pde, n, stencil_order, n_k, dist):
+        """Fused combine across GPUs (include/gbs.h gbs_bind_group_peers): a symmetric-memory
+        staging buffer per rank; every member of this rank's combine (the ranks holding the same
+        slab, one per sequence group) binds all members' workspaces and staging buffers."""
+        import torch
+        import torch.distributed as tdist
+        import torch.distributed._symmetric_memory as symm
+        plans = [gbs_plan(pde, n, stencil_order, n_k, dist["world"], r, dist.get("groups", 0))
+                 for r in range(dist["world"])]
+        me = plans[dist["rank"]]
+        members = sorted((p["my_group"], r) for r, p in enumerate(plans) if p["my_slab"] == me["my_slab"])
+        self.stage = symm.empty(max(gbs_stage_bytes(self.ctx), 1), dtype=torch.uint8, device="cuda")
+        self.stage_symm = symm.rendezvous(self.stage, tdist.group.WORLD)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        ws_ptrs, st_ptrs = self.symm.buffer_ptrs, self.stage_symm.buffer_ptrs
+        gbs_bind_group_peers(self.ctx, [ws_ptrs[r] for _, r in members], [st_ptrs[r] for _, r in members])
+
+    def _peer_workspace(self, pde, n, stencil_order, n_k, dist, nbytes, halos=True):
         """Peer halo pushes across GPUs (include/gbs.h gbs_bind_peers): the workspace is torch
         symmetric memory, every rank's mapped into every other; the neighbours are the ranks
         holding slab my_slab -/+ 1 of the same sequence group (collective over all ranks)."""
@@ -428,7 +450,8 @@ class Stepper:
         torch.cuda.synchronize()
         tdist.barrier()                          # every rank's flags are zeroed before any push
         ptrs = self.symm.buffer_ptrs
-        gbs_bind_peers(self.ctx, ptrs[lo], ptrs[hi])
+        if halos:
+            gbs_bind_peers(self.ctx, ptrs[lo], ptrs[hi])
         return ws
 
     def write(self, y):
@@ -466,6 +489,7 @@ class Stepper:
             gbs_destroy(self.ctx)
             self.ctx = None
         self.workspace = None
+        self.stage = None
 
     def __enter__(self):
         return self
