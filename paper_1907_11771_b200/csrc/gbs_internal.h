@@ -191,6 +191,8 @@ struct gbs_ctx {
     int nbuf = 4;                     // state buffers per slab: Y, ACC + 2 or 4 level buffers
     int zchunk_opt = 0;
     int zchunk_pair_opt = 0;          // planes per CTA of the two-substep kernel (0 = zchunk, else 256)
+    int zchunk_fin_opt = 0;           // the same for its LF + final pass only (0 = as above)
+    int hint_fin_opt = 11;            // L2 policy bits of the LF + final pass (PairArgs::hint)
     int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
     int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
     bool use_half = true;             // leap-frog pairs as two single-stencil-field launches, FE

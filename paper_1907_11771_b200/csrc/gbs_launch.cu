@@ -504,10 +504,11 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     // keeps >= 8 waves (C4 at 256 planes: 3.5 waves, 5% slower than 128)
     const int64_t tiles = (c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY);
     const int zauto = tiles * ((hi - lo + 255) / 256) >= 8LL * c->sms ? 256 : 128;
-    const int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : zauto;
+    int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : zauto;
+    if (!lf && c->zchunk_fin_opt > 0) zc = c->zchunk_fin_opt;
     a.zchunk = (int)std::min<int64_t>(zc, hi - lo);
     a.band = tile_band(c, c->n[0] / gbs::tma::TX);
-    a.hint = c->hint_opt;
+    a.hint = lf ? c->hint_opt : c->hint_fin_opt;
     dim3 grid((unsigned)((c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY)), 1u,
               (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
     face_chunks(lo, hi, gap, a.zchunk, a.zskip, grid.z);
