@@ -176,6 +176,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "l2hint") { c->hint_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "l2hint_step") { c->hint_step_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "band") { c->band_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "fin_ws") { c->fin_ws = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "zchunk_fin") { c->zchunk_fin_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "l2hint_fin") { c->hint_fin_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "zchunk_pair") { c->zchunk_pair_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }

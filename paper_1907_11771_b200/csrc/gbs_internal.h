@@ -193,6 +193,7 @@ struct gbs_ctx {
     int zchunk_pair_opt = 0;          // planes per CTA of the two-substep kernel (0 = zchunk, else 256)
     int zchunk_fin_opt = 0;           // the same for its LF + final pass only (0 = as above)
     int hint_fin_opt = 11;            // L2 policy bits of the LF + final pass (PairArgs::hint)
+    bool fin_ws = false;              // LF + final pass with specialised warps (wave3d_fin_ws_tma)
     int hint_opt = 11;                // pair kernel L2 policy bits (PairArgs::hint)
     int hint_step_opt = 0;            // single-step 3-D TMA kernel L2 policy bits (Wave3DArgs::hint)
     bool use_half = true;             // leap-frog pairs as two single-stencil-field launches, FE
