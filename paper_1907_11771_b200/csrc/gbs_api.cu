@@ -94,6 +94,9 @@ void gbs_destroy(gbs_ctx* c) {
     if (c->h2d) { cudaStreamSynchronize(c->h2d); cudaStreamDestroy(c->h2d); }
     if (c->cstream) { cudaStreamSynchronize(c->cstream); cudaStreamDestroy(c->cstream); }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->stream2) { cudaStreamSynchronize(c->stream2); cudaStreamDestroy(c->stream2); }
+    for (cudaEvent_t e : {c->ev_fork2, c->ev_join2, c->ev_fin})
+        if (e) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->d2h) { cudaStreamSynchronize(c->d2h); cudaStreamDestroy(c->d2h); }
     for (cudaEvent_t e : {c->ev_in_ready, c->ev_in_free, c->ev_out_ready, c->ev_out_free})
@@ -176,6 +179,10 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "l2hint") { c->hint_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "l2hint_step") { c->hint_step_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "band") { c->band_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "streams") {
+        if (value != 1 && value != 2) return fail(c, GBS_E_INVAL, "streams must be 1 or 2");
+        c->n_streams = (int)value; drop_graphs(); return GBS_OK;
+    }
     if (k == "fin_ws") { c->fin_ws = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "zchunk_fin") { c->zchunk_fin_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "l2hint_fin") { c->hint_fin_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }

@@ -373,6 +373,19 @@ static int enqueue_macro(gbs_ctx* c, double H) {
     bool fused2d = fused_path(c) && c->use_fuse2d && c->pde == GBS_ACOUSTIC2D;
     for (const auto& s : c->slab)                  // the chain kernels work in whole 32-row bands
         if (s.nz % gbs::tma::AC2_BH) fused2d = false;
+    // two sequence streams: single-substep paths on one slab with 6 state buffers (2-D TMA grids)
+    const bool two = c->n_streams == 2 && !fused && !fused2d && c->nbuf >= 6 && c->slabs * c->loopback == 1 &&
+                     !c->time_kernels && c->my_seq.size() > 1;
+    if (two) {
+        if (!c->stream2) {
+            CU(c, cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+            CU(c, cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
+            CU(c, cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming));
+            CU(c, cudaEventCreateWithFlags(&c->ev_fin, cudaEventDisableTiming));
+        }
+        CU(c, cudaEventRecord(c->ev_fork2, c->stream));
+        CU(c, cudaStreamWaitEvent(c->stream2, c->ev_fork2, 0));
+    }
     for (size_t q = 0; q < c->my_seq.size(); ++q) {
         const int k = c->my_seq[q];
         const int n = c->nk_all[k];
@@ -444,17 +457,39 @@ static int enqueue_macro(gbs_ctx* c, double H) {
             first = false;
             continue;
         }
-        if ((rc = step(c, 1, {Y, Y, B, gbs::MODE_FE, h, 0.0, false}))) return rc;            // y1
-        if ((rc = step(c, 0, {B, Y, C, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;      // y2
-        int prev = B, cur = C;
+        // two streams (option "streams"): sequence q on stream q % 2 with its own level buffers
+        // ({2,3} or {4,5}); the final passes stay in ascending n_k order (each waits for the
+        // previous one's event), so the accumulation order -- and the result -- is unchanged
+        const bool alt = two && (q % 2 == 1);
+        const int b1 = alt ? 4 : B, b2 = alt ? 5 : C;
+        cudaStream_t main_stream = c->stream;
+        if (alt) c->stream = c->stream2;
+        if ((rc = step(c, 1, {Y, Y, b1, gbs::MODE_FE, h, 0.0, false}))) { c->stream = main_stream; return rc; }
+        if ((rc = step(c, 0, {b1, Y, b2, gbs::MODE_LF, 2.0 * h, 0.0, false}))) { c->stream = main_stream; return rc; }
+        int prev = b1, cur = b2;
         for (int i = 2; i <= n - 1; ++i) {                                                    // y3..yN
-            if ((rc = step(c, 0, {cur, prev, prev, gbs::MODE_LF, 2.0 * h, 0.0, false}))) return rc;
+            if ((rc = step(c, 0, {cur, prev, prev, gbs::MODE_LF, 2.0 * h, 0.0, false}))) { c->stream = main_stream; return rc; }
             std::swap(prev, cur);
         }
         StepOperands fin{cur, prev, ACC, first ? gbs::MODE_FIN0 : gbs::MODE_FINACC, h,
                          0.5 * c->wk_all[k], last};
-        if ((rc = step(c, 2, fin))) return rc;
+        if (two && !first) {
+            cudaError_t e = cudaStreamWaitEvent(c->stream, c->ev_fin, 0);
+            if (e != cudaSuccess) { c->stream = main_stream; return fail(c, GBS_E_CUDA, "stream wait: %s", cudaGetErrorString(e)); }
+        }
+        rc = step(c, 2, fin);
+        if (!rc && two) {
+            cudaError_t e = cudaEventRecord(c->ev_fin, c->stream);
+            if (e != cudaSuccess) rc = fail(c, GBS_E_CUDA, "event record: %s", cudaGetErrorString(e));
+        }
+        c->stream = main_stream;
+        if (rc) return rc;
         first = false;
+    }
+    if (two) {
+        // join the second stream (its last final pass precedes the main stream's, or is it)
+        CU(c, cudaEventRecord(c->ev_join2, c->stream2));
+        CU(c, cudaStreamWaitEvent(c->stream, c->ev_join2, 0));
     }
     if (c->groups > 1 && !combined) {
         // Y <- sum over the sequence groups of their w-scaled partial sums

@@ -245,6 +245,20 @@ def test_specialised_warp_final_pass_bitwise(torch_cuda, cfg, n, opts):
     assert_parity(a[0], o[0], what=f"fin_ws {cfg} {n} {opts}")
 
 
+@pytest.mark.parametrize("cfg,n,opts", [("c2", (128, 64, 1), {}), ("c3", (192, 96, 1), {}),
+                                        ("c2", (64, 48, 1), {"graph": 0}), ("c4", (64, 32, 24), {"fuse": 0})])
+def test_two_sequence_streams_bitwise(torch_cuda, cfg, n, opts):
+    """Sequences alternating over two CUDA streams (option streams = 2) with the final passes
+    kept in ascending n_k order: the same arithmetic and accumulation order -> bit-identical."""
+    w = reduced(cfg, n, macro_steps=3, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 3, opts=dict(opts, streams=2))
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 3, opts=dict(opts, streams=1))
+    assert np.array_equal(a[0], b[0])
+    o = run_oracle(w, y0, counts, wd, H, 3)
+    assert_parity(a[0], o[0], what=f"streams=2 {cfg} {n} {opts}")
+
+
 @pytest.mark.parametrize("opts", [{"band": 1}, {"band": 2}, {"band": 3}, {"l2hint": 0},
                                   {"l2hint": 15, "l2hint_step": 11}])
 def test_tile_order_and_cache_policies_do_not_change_results(torch_cuda, opts):
