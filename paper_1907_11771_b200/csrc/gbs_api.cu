@@ -183,7 +183,6 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
         if (value != 1 && value != 2) return fail(c, GBS_E_INVAL, "streams must be 1 or 2");
         c->n_streams = (int)value; drop_graphs(); return GBS_OK;
     }
-    if (k == "fin_ws") { c->fin_ws = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "zchunk_fin") { c->zchunk_fin_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "l2hint_fin") { c->hint_fin_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "zchunk_pair") { c->zchunk_pair_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }

@@ -193,7 +193,6 @@ struct gbs_ctx {
     int zchunk_pair_opt = 0;          // planes per CTA of the two-substep kernel (0 = zchunk, else 256)
     int zchunk_fin_opt = 0;           // the same for its LF + final pass only (0 = as above)
     int hint_fin_opt = 11;            // L2 policy bits of the LF + final pass (PairArgs::hint)
-    bool fin_ws = false;              // LF + final pass with specialised warps (wave3d_fin_ws_tma)
     int n_streams = 1;                // sequence streams (option "streams": 1 or 2)
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr, ev_fin = nullptr;

@@ -196,7 +196,7 @@ static cudaError_t launch_wave3d_tma(const gbs::tma::Maps& m, const gbs::Wave3DA
 }
 template <int R, int MODEB, bool SLAB>
 static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::PairArgs& a, int zbase, dim3 grid,
-                                   cudaStream_t st, const gbs::tma::PeerPush* peer, bool ws = false) {
+                                   cudaStream_t st, const gbs::tma::PeerPush* peer) {
     using L = gbs::tma::PairLayout<R, MODEB>;
     const dim3 block(32, gbs::tma::TY / 2);
     if constexpr (SLAB) {
@@ -209,15 +209,6 @@ static cudaError_t launch_pair_tma(const gbs::tma::PairMaps& m, const gbs::tma::
         }
     }
     if (peer) return cudaErrorNotSupported;
-    if constexpr (MODEB != gbs::MODE_LF) {
-        if (ws) {
-            auto k = gbs::tma::wave3d_fin_ws_tma<R, MODEB, SLAB>;
-            cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), L::bytes);
-            if (e != cudaSuccess) return e;
-            k<<<grid, dim3(32, gbs::tma::TY), L::bytes, st>>>(m, a, zbase);
-            return cudaSuccess;
-        }
-    }
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(gbs::tma::wave3d_pair_tma<R, MODEB, SLAB>), L::bytes);
     if (e != cudaSuccess) return e;
     gbs::tma::wave3d_pair_tma<R, MODEB, SLAB><<<grid, block, L::bytes, st>>>(m, a, zbase, gbs::tma::PeerPush{});
@@ -534,8 +525,8 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
 #define PR(RR, SL)                                                                                          \
     switch (op.modeB) {                                                                                     \
         case gbs::MODE_LF: e = launch_pair_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream, peer); break;     \
-        case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream, peer, c->fin_ws); break; \
-        default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream, peer, c->fin_ws); break;           \
+        case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream, peer); break; \
+        default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream, peer); break;           \
     }
     if (c->R == 2) { if (slab) { PR(2, true) } else { PR(2, false) } }
     else { if (slab) { PR(4, true) } else { PR(4, false) } }

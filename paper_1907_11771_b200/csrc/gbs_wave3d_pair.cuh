@@ -60,7 +60,7 @@ struct PairLayout {
     static constexpr int O_SV = 2 * TILE + 2 * PWT, O_PV = 2 * TILE + 3 * PWT, O_AC = 2 * TILE + 4 * PWT;
     static constexpr int STAGE = 2 * TILE + (4 + NACC) * PWT;
     static constexpr size_t stage_doubles = (size_t)D * STAGE;
-    static constexpr size_t bytes = stage_doubles * 8 + (3 * D + 1) * 8;
+    static constexpr size_t bytes = stage_doubles * 8 + (2 * D + 1) * 8;
     static constexpr uint32_t stage_bytes = STAGE * 8;
     static_assert((TILE * 8) % 128 == 0 && (PWT * 8) % 128 == 0, "TMA destinations need 128 B alignment");
 };
@@ -332,251 +332,6 @@ wave3d_pair_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int 
     }
     if constexpr (MODEB != MODE_LF)
         if (bad && A.nonfinite) *A.nonfinite = 1;
-}
-
-// ---------------------------------------------------------------------------
-// The LF + final pass with specialised warps (option "fin_ws").  The pass needs both
-// laplacians -- lap(S_u) for v_N (the last step of one leap-frog chain) and lap(U) for the
-// averaging (the other chain's level N) -- so it cannot split into two single-field launches
-// without 24 more bytes per point.  Instead warps 0-7 carry the S_u queue and
-// form v_N = P_v + cfA lap(S_u), which they store over P_v's own points in the stage (read
-// only there, by the same thread, a moment earlier), and warps 8-15 carry the U queue and,
-// once an mbarrier says v_N of that stage is in, form the averaged, weighted contributions
-//   acc_u (+)= wh (S_u + U + cfB v_N),   acc_v (+)= wh (S_v + v_N + cfB lap(U)).
-// One register queue per warp: 16 warps at <= 128 registers instead of 8 at 240, the same
-// stage layout, HBM bytes and operations (bit-identical to wave3d_pair_tma).
-// ---------------------------------------------------------------------------
-template <int R, int MODEB, bool SLAB>
-__global__ void __launch_bounds__(512, 1)
-wave3d_fin_ws_tma(const __grid_constant__ PairMaps M, const PairArgs A, const int zbase) {
-    using L = PairLayout<R, MODEB>;
-    constexpr int D = L::D, STAGE = L::STAGE;
-    constexpr int NW = TY;                     // 16 warps: 8 per role, 2 rows x 2 columns per thread
-    constexpr int Q = 2 * R + 1;
-    extern __shared__ __align__(128) double smem[];
-    double* stages = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::stage_doubles);
-    uint64_t* empty = full + D;
-    uint64_t* vready = empty + D;              // v_N of the stage is in (8 arrivals)
-
-    const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
-    const bool roleA = ty < NW / 2;            // S_u queue, v_N
-    const int rr = roleA ? ty : ty - NW / 2;
-    const int nx = A.nx, ny = A.ny, nz = A.nz;
-    int xt, yt;
-    tile_of(blockIdx.x, nx / TX, ny / TY, A.band, xt, yt);
-    const int x0 = xt * TX, y0 = yt * TY;
-    const int z0 = A.zlo + blockIdx.z * A.zchunk + (blockIdx.z ? A.zskip : 0);
-    const int niter = min(A.zchunk, A.zhi - z0);
-    auto zc = [&](int z) -> int {
-        if constexpr (SLAB) return z + zbase;
-        else return wrap_once(z, nz);
-    };
-    const int64_t plane = A.plane;
-    const int r0 = 2 * rr;                     // the thread's rows r0, r0 + 1 of the tile
-    const int64_t own = (int64_t)(y0 + r0) * nx + x0 + 2 * tx;
-    auto zoff = [&](int z) -> int64_t {
-        if constexpr (SLAB) return (int64_t)z * plane;
-        else return (int64_t)wrap_once(z, nz) * plane;
-    };
-    const bool producer = (ty == 0 && lane == 0);
-    const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
-    const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
-
-    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
-    auto ld = [&](void* dst, const CUtensorMap* m, int x, int y, int z, uint64_t* bar, int bit, uint64_t pol) {
-        if (A.hint & bit) tma_load_3d_hint(dst, m, x, y, z, bar, pol);
-        else tma_load_3d(dst, m, x, y, z, bar);
-    };
-    auto load_tile = [&](double* dst, const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int z,
-                         uint64_t* bar) {
-        ld(dst, b, x0, ytop, z, bar, 4, pol_first);
-        ld(dst + R * TX, a, x0, y0, z, bar, 4, pol_first);
-        ld(dst + (R + TY) * TX, b, x0, ybot, z, bar, 4, pol_first);
-        ld(dst + L::CENTER, c, xl, y0, z, bar, 4, pol_first);
-        ld(dst + L::CENTER + L::STRIP, c, xr, y0, z, bar, 4, pol_first);
-    };
-    auto issue_stage = [&](int i) {
-        const int s = i % D;
-        if (i >= D) mbar_wait(&empty[s], (uint32_t)(((i / D) - 1) & 1));
-        mbar_expect_tx(&full[s], L::stage_bytes);
-        double* st = stages + (size_t)s * STAGE;
-        const int z = zc(z0 + i), zf = zc(z0 + i + R);
-        load_tile(st, &M.su_a, &M.su_b, &M.su_c, z, &full[s]);
-        load_tile(st + L::O_UT, &M.u_a, &M.u_b, &M.u_c, z, &full[s]);
-        ld(st + L::O_SUF, &M.su_a, x0, y0, zf, &full[s], 1, pol_last);
-        ld(st + L::O_UF, &M.u_a, x0, y0, zf, &full[s], 1, pol_last);
-        ld(st + L::O_SV, &M.sv, x0, y0, z, &full[s], 2, pol_first);
-        ld(st + L::O_PV, &M.pv, x0, y0, z, &full[s], 2, pol_first);
-        if constexpr (MODEB == MODE_FINACC) {
-            ld(st + L::O_AC, &M.acc_u, x0, y0, z, &full[s], 2, pol_first);
-            ld(st + L::O_AC + L::PWT, &M.acc_v, x0, y0, z, &full[s], 2, pol_first);
-        }
-    };
-
-    if (producer) {
-        for (int s = 0; s < D; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
-            mbar_init(&vready[s], NW / 2);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (producer) {
-        prefetch_map(&M.su_a); prefetch_map(&M.su_b); prefetch_map(&M.su_c);
-        prefetch_map(&M.u_a); prefetch_map(&M.u_b); prefetch_map(&M.u_c);
-        prefetch_map(&M.sv); prefetch_map(&M.pv);
-        if constexpr (MODEB == MODE_FINACC) { prefetch_map(&M.acc_u); prefetch_map(&M.acc_v); }
-        for (int i = 0; i < D - 1 && i < niter; ++i) issue_stage(i);
-    }
-    // this role's field: S_u (A) or U (B); register queue at planes z-R .. z+R
-    const double* X = roleA ? A.Su : A.U;
-    const int o_tile = roleA ? 0 : L::O_UT, o_front = roleA ? L::O_SUF : L::O_UF;
-    double q[Q][4];
-#pragma unroll
-    for (int j = 0; j < 2 * R; ++j) {
-        const int64_t oz = zoff(z0 - R + j);
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const double2 t = __ldg(reinterpret_cast<const double2*>(X + oz + own + (int64_t)r * nx));
-            q[j][2 * r] = t.x; q[j][2 * r + 1] = t.y;
-        }
-    }
-    int woff[2][R + 1];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int k = 0; k <= R; ++k) {
-            const int col = 2 * tx - R + 2 * k, row = r0 + r;
-            woff[r][k] = col < 0 ? L::CENTER + row * R + (col + R)
-                       : col >= TX ? L::CENTER + L::STRIP + row * R + (col - TX)
-                                   : (R + row) * TX + col;
-        }
-    const int crow0 = (R + r0) * TX + 2 * tx;
-
-    bool bad = false;
-    for (int i = 0; i < niter; ++i) {
-        const int s = i % D;
-        if (producer && i + D - 1 < niter) issue_stage(i + D - 1);
-        mbar_wait(&full[s], (uint32_t)((i / D) & 1));
-        double* st = stages + (size_t)s * STAGE;
-        const double* tile = st + o_tile;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const double2 f = *reinterpret_cast<const double2*>(st + o_front + (r0 + r) * TX + 2 * tx);
-            q[2 * R][2 * r] = f.x; q[2 * R][2 * r + 1] = f.y;
-        }
-        // lap at the 4 points, the coupled kernel's sums in its order (wave3d_pair_tma: lap4)
-        double lap[4], cen[4];
-        {
-            double lx[4], ly[4], lz[4];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                double xw[2 * R + 2];
-#pragma unroll
-                for (int k = 0; k <= R; ++k) {
-                    if (k == R / 2) {
-                        xw[2 * k] = q[R][2 * r]; xw[2 * k + 1] = q[R][2 * r + 1];
-                        continue;
-                    }
-                    const double2 a = *reinterpret_cast<const double2*>(tile + woff[r][k]);
-                    xw[2 * k] = a.x; xw[2 * k + 1] = a.y;
-                }
-#pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    const int p = 2 * r + v;
-                    cen[p] = xw[R + v];
-                    lx[p] = FD<R>::b0() * xw[R + v];
-#pragma unroll
-                    for (int j = 1; j <= R; ++j) lx[p] = fma(FD<R>::b(j), xw[R + v + j] + xw[R + v - j], lx[p]);
-                    ly[p] = FD<R>::b0() * xw[R + v];
-                    lz[p] = ly[p];
-                }
-            }
-            double prev_up[2], prev_dn[2];
-#pragma unroll
-            for (int j = 1; j <= R; ++j) {
-                const double2 u = *reinterpret_cast<const double2*>(tile + crow0 - j * TX);
-                const double2 d = *reinterpret_cast<const double2*>(tile + crow0 + (1 + j) * TX);
-                const double up0[2] = {u.x, u.y}, dn1[2] = {d.x, d.y};
-#pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    const double dn0 = (j == 1) ? cen[2 + v] : prev_dn[v];
-                    const double up1 = (j == 1) ? cen[v] : prev_up[v];
-                    ly[v] = fma(FD<R>::b(j), dn0 + up0[v], ly[v]);
-                    ly[2 + v] = fma(FD<R>::b(j), dn1[v] + up1, ly[2 + v]);
-                    prev_up[v] = up0[v];
-                    prev_dn[v] = dn1[v];
-                }
-            }
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-#pragma unroll
-                for (int j = 1; j <= R; ++j) lz[p] = fma(FD<R>::b(j), q[R + j][p] + q[R - j][p], lz[p]);
-                lap[p] = fma(A.sx2, lx[p], fma(A.sy2, ly[p], A.sz2 * lz[p]));
-            }
-        }
-        if (roleA) {
-            // v_N = P_v + cfA lap(S_u), stored over P_v's own points of the stage
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                double2* pv = reinterpret_cast<double2*>(st + L::O_PV + (r0 + r) * TX + 2 * tx);
-                const double2 b = *pv;
-                *pv = make_double2(combine<MODE_LF>(b.x, 0.0, lap[2 * r], 0.0, A.cfA, 0.0),
-                                   combine<MODE_LF>(b.y, 0.0, lap[2 * r + 1], 0.0, A.cfA, 0.0));
-            }
-            __syncwarp();
-            if (lane == 0) { mbar_arrive(&vready[s]); mbar_arrive(&empty[s]); }
-        } else {
-            double csv[4], cau[4] = {0, 0, 0, 0}, cav[4] = {0, 0, 0, 0}, xs[4];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int po = (r0 + r) * TX + 2 * tx;
-                const double2 a = *reinterpret_cast<const double2*>(st + L::O_SV + po);
-                const double2 u = *reinterpret_cast<const double2*>(st + (R + r0 + r) * TX + 2 * tx);   // S_u own
-                csv[2 * r] = a.x; csv[2 * r + 1] = a.y; xs[2 * r] = u.x; xs[2 * r + 1] = u.y;
-                if constexpr (MODEB == MODE_FINACC) {
-                    const double2 c = *reinterpret_cast<const double2*>(st + L::O_AC + po);
-                    const double2 d = *reinterpret_cast<const double2*>(st + L::O_AC + L::PWT + po);
-                    cau[2 * r] = c.x; cau[2 * r + 1] = c.y; cav[2 * r] = d.x; cav[2 * r + 1] = d.y;
-                }
-            }
-            mbar_wait(&vready[s], (uint32_t)((i / D) & 1));
-            double va[4];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const double2 b = *reinterpret_cast<const double2*>(st + L::O_PV + (r0 + r) * TX + 2 * tx);
-                va[2 * r] = b.x; va[2 * r + 1] = b.y;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            double ub[4], vb[4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                ub[p] = combine<MODEB>(xs[p], cen[p], va[p], cau[p], A.cfB, A.wh);     // acc_u
-                vb[p] = combine<MODEB>(csv[p], va[p], lap[p], cav[p], A.cfB, A.wh);    // acc_v
-                bad |= !isfinite(ub[p]) || !isfinite(vb[p]);
-            }
-            const int64_t oz = zoff(z0 + i);
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int64_t o = oz + own + (int64_t)r * nx;
-                if (A.hint & 8) {
-                    __stcs(reinterpret_cast<double2*>(A.Bu + o), make_double2(ub[2 * r], ub[2 * r + 1]));
-                    __stcs(reinterpret_cast<double2*>(A.Bv + o), make_double2(vb[2 * r], vb[2 * r + 1]));
-                } else {
-                    *reinterpret_cast<double2*>(A.Bu + o) = make_double2(ub[2 * r], ub[2 * r + 1]);
-                    *reinterpret_cast<double2*>(A.Bv + o) = make_double2(vb[2 * r], vb[2 * r + 1]);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 2 * R; ++j)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) q[j][p] = q[j + 1][p];
-    }
-    if (bad && A.nonfinite) *A.nonfinite = 1;
 }
 
 }  // namespace tma

@@ -230,21 +230,6 @@ def test_half_kernels_bitwise_equal_coupled_pair(torch_cuda, cfg, n, opts):
     assert_parity(a[0], o[0], what=f"half kernels {cfg} {n} {opts}")
 
 
-@pytest.mark.parametrize("cfg,n,opts", [("c5", (128, 32, 40), {}), ("c4", (64, 16, 9), {}),
-                                        ("c5", (64, 48, 48), {"loopback": 3}),
-                                        ("c4", (64, 32, 30), {"loopback": 2, "overlap": 0, "zchunk_fin": 7})])
-def test_specialised_warp_final_pass_bitwise(torch_cuda, cfg, n, opts):
-    """The LF + final pass with specialised warps (wave3d_fin_ws_tma, option fin_ws): the same
-    operations in the same order as the coupled kernel -> bit-identical, and the oracle's."""
-    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
-    counts, wd, H = scheme_for(w, "nonzero8")
-    y0, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fin_ws=1))
-    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fin_ws=0))
-    assert np.array_equal(a[0], b[0])
-    o = run_oracle(w, y0, counts, wd, H, 2)
-    assert_parity(a[0], o[0], what=f"fin_ws {cfg} {n} {opts}")
-
-
 @pytest.mark.parametrize("cfg,n,opts", [("c2", (128, 64, 1), {}), ("c3", (192, 96, 1), {}),
                                         ("c2", (64, 48, 1), {"graph": 0}), ("c4", (64, 32, 24), {"fuse": 0})])
 def test_two_sequence_streams_bitwise(torch_cuda, cfg, n, opts):
