@@ -14,6 +14,7 @@
 #include "gbs_wave3d_tma.cuh"     // substep modes and the TMA tile (no launches here)
 #include "gbs_acoustic2d_pair.cuh"  // AC2_BH (band rows of the 2-D chain kernels)
 #include "gbs_wave3d_half.cuh"      // HALF_LF / HALF_FE
+#include "gbs_wave3d_pair.cuh"      // MODE_FEA
 
 // ---------------------------------------------------------------------------
 // halo exchange of buffer b's fields in `mask` (bit f = field f; 0 = the fields
@@ -413,7 +414,14 @@ static int enqueue_macro(gbs_ctx* c, double H) {
             // u-levels rotate through (2,0)/(3,0) and (4,0)/(5,0); v_{odd} stays in
             // (2,1) and v_{even} in (3,1), both updated in place (pointwise reads).
             const bool half = half_eligible(c);
-            if (half && c->half_fe) {
+            // FE fused with chain A's first step (option "fea"; gbs_wave3d_pair.cuh MODE_FEA)
+            const bool fea = half && c->use_fea && n >= 4;
+            if (fea) {
+                PairOperands fe{Slot{Y, 1}, Slot{Y, 0}, Slot{Y, 1}, Slot{Y, 1},
+                                Slot{3, 1}, Slot{4, 0}, Slot{2, 1}, Slot{3, 0},
+                                gbs::tma::MODE_FEA, h, 2.0 * h, 0.0, false};
+                if ((rc = pair_step(c, 7, fe))) return rc;     // v2, u3 | v1, u2
+            } else if (half && c->half_fe) {
                 // v1 = v0 + h lap(u0), u2 = u0 + 2h v1, u1 = u0 + h v0 (the FE kernel's values)
                 HalfOperands fe{gbs::tma::HALF_FE, Slot{Y, 0}, Slot{Y, 1}, Slot{2, 1}, Slot{3, 0}, Slot{2, 0},
                                 h, 2.0 * h};
@@ -437,7 +445,8 @@ static int enqueue_macro(gbs_ctx* c, double H) {
                         ha.c1 = op.cfA; ha.c2 = op.cfB;
                         HalfOperands hb{gbs::tma::HALF_LF, op.U, op.Sv, op.Bv, op.Cu};
                         hb.c1 = op.cfB; hb.c2 = op.cfA;
-                        if ((rc = half_step(c, 6, ha)) || (rc = half_step(c, 6, hb))) return rc;
+                        if (!(fea && p == 0) && (rc = half_step(c, 6, ha))) return rc;   // FEA did A0
+                        if ((rc = half_step(c, 6, hb))) return rc;
                     } else if ((rc = pair_step(c, 3, op))) {
                         return rc;
                     }

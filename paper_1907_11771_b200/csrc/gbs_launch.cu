@@ -479,7 +479,7 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
     // slab kernels read ghost planes refreshed from neighbours; one slab (2-D TMA grids keep
     // ghost rows for the two-substep kernels) wraps periodically like a plain grid
     const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
-    const bool lf = op.modeB == gbs::MODE_LF;
+    const bool lf = op.modeB == gbs::MODE_LF || op.modeB == gbs::tma::MODE_FEA;   // four level outputs
     gbs::tma::PairArgs a{};
     if (lf) {
         a.Av = field_ptr(c, s, op.Av.b, op.Av.f);
@@ -525,6 +525,7 @@ int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t
 #define PR(RR, SL)                                                                                          \
     switch (op.modeB) {                                                                                     \
         case gbs::MODE_LF: e = launch_pair_tma<RR, gbs::MODE_LF, SL>(m, a, zbase, grid, c->stream, peer); break;     \
+        case gbs::tma::MODE_FEA: e = launch_pair_tma<RR, gbs::tma::MODE_FEA, SL>(m, a, zbase, grid, c->stream, peer); break; \
         case gbs::MODE_FIN0: e = launch_pair_tma<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream, peer); break; \
         default: e = launch_pair_tma<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream, peer); break;           \
     }

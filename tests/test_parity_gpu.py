@@ -230,6 +230,25 @@ def test_half_kernels_bitwise_equal_coupled_pair(torch_cuda, cfg, n, opts):
     assert_parity(a[0], o[0], what=f"half kernels {cfg} {n} {opts}")
 
 
+@pytest.mark.parametrize("cfg,n,opts", [("c5", (128, 64, 40), {}), ("c4", (64, 48, 30), {}),
+                                        ("c5", (64, 64, 48), {"loopback": 3}), ("c4", (64, 16, 9), {}),
+                                        ("c4", (64, 32, 24), {"loopback": 2, "overlap": 0, "graph": 0})])
+def test_fe_fused_with_first_chain_step(torch_cuda, cfg, n, opts):
+    """Option fea: the FE fused with the first step of one leap-frog chain (lap(u_1) by
+    linearity, gbs_wave3d_pair.cuh MODE_FEA) -- a rounding-level change, so against the oracle
+    and the unfused path within the parity bar, and one launch fewer per sequence with n >= 4."""
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    y0, a, ia = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1))
+    _, b, ib = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=0))
+    o = run_oracle(w, y0, counts, wd, H, 2)
+    assert_parity(a[0], o[0], what=f"fea {cfg} {n} {opts}")
+    assert_parity(a[0], b[0], what=f"fea vs unfused {cfg} {n} {opts}")
+    slabs = opts.get("loopback", 1)
+    per = 1 if (slabs == 1 or not opts.get("overlap", 1)) else 2
+    assert ib["kernel_launches"] - ia["kernel_launches"] == 2 * slabs * per * sum(1 for k in counts if k >= 4)
+
+
 @pytest.mark.parametrize("cfg,n,opts", [("c2", (128, 64, 1), {}), ("c3", (192, 96, 1), {}),
                                         ("c2", (64, 48, 1), {"graph": 0}), ("c4", (64, 32, 24), {"fuse": 0})])
 def test_two_sequence_streams_bitwise(torch_cuda, cfg, n, opts):
