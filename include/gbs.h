@@ -306,6 +306,10 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        one register queue per CTA (default 1; 0 = the coupled pair kernel;
  *                        peer pushes always use the coupled kernel)
  *   "half_fe"      1/0   the forward-Euler substep through the same kernel (default 0)
+ *   "fea"          1/0   sequences with n_k >= 4 on that path: the forward-Euler substep fused with
+ *                        the first step of the u_1 leap-frog chain in one two-field pass (u_0, v_0 in;
+ *                        v_1, u_2, v_2, u_3 out: 48 B per point instead of 40 + 32), lap(u_1) formed
+ *                        as lap(u_0) + h lap(v_0) -- a rounding-level change; default 1)
  *   "half_tall"    1/0   64 x 32 tiles for the half kernel when ny % 32 == 0 (default 1)
  *   "half_rpt"     2/4   rows per thread of the tall half kernel (16 or 8 warps; default 4)
  *   "l2hint_half"  bits  half kernel: 1 centre boxes evict_last, 2 streaming loads of the
