@@ -386,7 +386,7 @@ def run_ours(a):
             4: ("leap-frog + final substep in one pass", 48 * F),
             5: ("whole-run cluster kernel", 24 * F * S * run_len),
             6: ("one single-stencil-field half of a two-substep pass", 24 * F),
-            7: ("unused", 0)}
+            7: ("forward Euler + the first step of one leap-frog chain in one pass", 16 * F + 24 * F)}
     # bytes per point the kernel itself must read + write once (its own minimum HBM
     # traffic): the two-substep 3-D kernel moves S_u, U, S_v, P_v in and A_v, B, C_u out
     # (gbs_wave3d_pair.cuh) = 64 B instead of the metric's 2 x 24F = 96 B, and the FE
@@ -395,7 +395,7 @@ def run_ours(a):
     # half (class 6): reads X, P and writes O1, O2 = 32 B (its 24F = 48 B algorithmic figure: each of
     # the pair's two substeps is completed by one of the two halves); LF + FIN pass: 32 B of levels
     # + 16 B accumulator in, 16 B out (FIN0: no accumulator read; counted as FINACC)
-    MOVED = {0: 24 * F, 1: 16 * F + (8 if fused3d else 0), 3: 64, 4: 64, 6: 32}
+    MOVED = {0: 24 * F, 1: 16 * F + (8 if fused3d else 0), 3: 64, 4: 64, 6: 32, 7: 48}
     dom = max(ktimes, key=lambda c: ktimes[c][0])
     dom_ms, dom_n = ktimes[dom]
     avg = dom_ms / max(dom_n, 1)
