@@ -866,6 +866,7 @@ def _random_cases(seed=20261020, count=14, include_1d=False):
         lb = int(rng.choice(lbs))
         opts = {"loopback": lb, "overlap": int(rng.integers(0, 2)), "graph": int(rng.integers(0, 2)),
                 "half": int(rng.integers(0, 2)), "half_rpt": int(rng.choice([2, 4])),
+                "fea": int(rng.integers(0, 2)), "streams": int(rng.choice([1, 1, 2])),
                 "fuse": int(rng.integers(0, 2)), "band": int(rng.choice([0, 1, 2])),
                 "zchunk": int(rng.choice([0, 0, 8, 17])), "zchunk_pair": int(rng.choice([0, 0, 5, 32])),
                 "l2hint": int(rng.choice([11, 0, 15]))}
