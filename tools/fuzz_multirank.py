@@ -35,11 +35,13 @@ for _ in range(count):
     groups = int(rng.choice(gs))
     slabs = world // groups
     if cfg in ("c4", "c5"):
-        nz = int(rng.choice([4, 6, 8, 12])) * slabs * 2
+        nz = max(int(rng.choice([4, 6, 8, 12])) * slabs * 2, 9 + (-9) % slabs)   # >= 2r + 1
         n = (int(rng.choice([64, 128, 40, 72])), int(rng.choice([16, 32, 36])), nz)
     elif cfg in ("c2", "c3"):
         R = 2 if cfg == "c2" else 4
         rows = int(rng.choice([R, 16, 24, 32]))
+        while rows * slabs < 2 * R + 1:                                           # >= 2r + 1
+            rows += R
         n = (int(rng.choice([64, 128, 96, 80])), rows * slabs, 1)
     else:
         n = (int(rng.choice([64, 256, 300])), 1, 1)
