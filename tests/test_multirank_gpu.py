@@ -234,3 +234,13 @@ def test_fused_combine_through_bound_peer_buffers(torch_cuda, world, groups):
     _, b, _ = run_ranks(torch_cuda, w, counts, wd, H, 2, world, groups, {"fused_combine": 0})
     for r in range(world):
         assert np.array_equal(a[r], b[r])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world,groups,fused", [(8, 2, 1), (8, 1, 0), (4, 4, 1)])
+def test_c4_full_size_multirank(torch_cuda, world, groups, fused):
+    """The C4 grid at full size (512^3, FD8, {2..12}, nonzero8) as 4-8 ranks (slabs of 64-512
+    planes, sequence groups, the fused combine) on one GPU, one macro step, full state."""
+    opts = {"fused_combine": fused} if groups > 1 else {}
+    rel, mmax = check(torch_cuda, "c4", (512, 512, 512), 1, world, groups, opts=opts)
+    assert rel <= TOL

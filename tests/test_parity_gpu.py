@@ -718,6 +718,24 @@ def test_2d_full_size_whole_run(torch_cuda, cfg):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("cfg,M", [("c2", 10), ("c3", 4)])
+def test_2d_full_size_nonzero_weights(torch_cuda, cfg, M):
+    """C2 / C3 at full size with the all-nonzero parity weights (fallback8 gives the
+    sequences 10 and 12 weight 0, so only a nonzero set shows a bug in them), full state."""
+    w = get_config(cfg).with_(weights="nonzero8")
+    counts, wd, H = scheme_for(get_config(cfg), "nonzero8")
+    gbs = gbs_mod()
+    y0 = make_ic(w)
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch_cuda.from_numpy(y0).cuda())
+        st.advance(M, H)
+        out = np.empty_like(y0)
+        st.read(out)
+    ref = C.advance(w.pde, w.order, y0, counts, wd, H, M)
+    assert_parity(out, ref, what=f"{cfg} full nonzero8, {M} macro steps")
+
+
+@pytest.mark.slow
 def test_c4_full_size_whole_run(torch_cuda):
     """The whole BASELINE.json C4 run (512^3, FD8, {2..12}, 10 macro steps; the two-substep
     TMA path) against the oracle over the full state after 5 and 10 macro steps (the oracle
