@@ -106,7 +106,7 @@ def check(torch, cfg, n, M, world, groups, wset="nonzero8", opts=None):
     rel, mrms, mmax = errors(outs[0], ref)
     record_parity(f"multirank {cfg} {n} {wset} world={world} groups={groups} {opts or {}}", rel, mrms, mmax)
     assert rel <= TOL and mmax <= TOL_ELEM, f"{cfg} {n} world={world} groups={groups}: rel L2 {rel:.3e}, max {mmax:.3e}"
-    single = run_single(torch, w, counts, wd, H, M, opts)
+    single = run_single(torch, w, counts, wd, H, M, {k: v for k, v in (opts or {}).items() if k != "fused_combine"})
     if groups == 1:
         assert np.array_equal(outs[0], single), "pure slabs must be bit-identical to one context"
     else:
