@@ -244,3 +244,46 @@ def test_c4_full_size_multirank(torch_cuda, world, groups, fused):
     opts = {"fused_combine": fused} if groups > 1 else {}
     rel, mmax = check(torch_cuda, "c4", (512, 512, 512), 1, world, groups, opts=opts)
     assert rel <= TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("groups,fused", [(1, 0)])
+def test_c5_full_size_eight_ranks_match_one_context(torch_cuda, groups, fused):
+    """The bench workload itself (C5: 1024^3, FD8, {2..16}, fallback8) as 8 ranks on one GPU --
+    the decomposition the 8-GPU bench runs (the planner's pure slabs of 128 planes) -- one macro
+    step, every rank's slab bit-identical to the one-context state.  (Sequence groups at this
+    size do not fit one GPU's memory: 8 ranks x 6 buffers x 4 GiB; C4 covers them at full size.)"""
+    from paper_1907_11771_b200 import gbs
+    torch = torch_cuda
+    w = get_config("c5")
+    counts, wd, H = scheme_for(w, "fallback8", "c5")
+    y0 = make_ic(w)
+    with gbs.Stepper(w.pde, w.n, w.order, counts, wd) as st:
+        st.write(torch.from_numpy(y0).cuda())
+        st.advance(1, H)
+        ref = np.empty_like(y0)
+        st.read(ref)
+    world = 8
+
+    def body(dist):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        opts = {"fused_combine": fused} if groups > 1 else {}
+        with gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist, stream=s.cuda_stream, **opts) as st:
+            info = st.info()
+            z0, nz = info["slab_z0"], info["slab_nz"]
+            st.write_slab(np.ascontiguousarray(y0[:, z0:z0 + nz]))
+            st.advance(1, H)
+            out = np.empty((2, nz) + y0.shape[2:], dtype=np.float64)
+            st.read_slab(out)
+            return z0, nz, out, info["groups"]
+
+    res = gbs.run_local_ranks(world, body, groups=groups)
+    for z0, nz, out, g in res:
+        assert g == groups
+        part = ref[:, z0:z0 + nz]
+        if groups == 1:
+            assert np.array_equal(out, part)
+        else:
+            rel, _, mmax = errors(out, part)
+            assert rel <= TOL and mmax <= TOL_ELEM
