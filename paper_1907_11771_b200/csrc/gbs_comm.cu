@@ -211,7 +211,7 @@ struct LocalComm final : Comm {
     }
     int bar(gbs_ctx* c) {
         if (!S->barrier())
-            return fail(c, GBS_E_NCCL, "local transport: a member rank did not reach the collective (300 s)");
+            return fail(c, GBS_E_NCCL, "local transport: a member rank failed or did not reach the collective (300 s)");
         return GBS_OK;
     }
     int group_start(gbs_ctx*) override {
@@ -332,6 +332,11 @@ struct LocalComm final : Comm {
         return bar(c);
     }
     gbs_ctx* member_ctx(int i) override { return (i >= 0 && i < size) ? S->ctx[i] : nullptr; }
+    void abort() override {
+        std::lock_guard<std::mutex> lk(S->mu);
+        S->broken = true;
+        S->cv.notify_all();
+    }
     void register_ctx(gbs_ctx* c) override { S->ctx[rank] = c; }
     int split(gbs_ctx* c, int color, int key, Comm** out) override {
         int rc;
@@ -406,6 +411,13 @@ int comm_nccl_self(gbs_ctx* c, Comm** out) {
     if (r) return fail(c, GBS_E_NCCL, "one-rank communicator: %s", A.GetErrorString(r));
     *out = new NcclComm(h, 0, 1);
     return GBS_OK;
+}
+
+int comm_abort_on_error(gbs_ctx* c, int rc) {
+    if (rc != GBS_OK && c && c->local_transport)
+        for (Comm* k : {c->comm_world, c->comm_slab, c->comm_group})
+            if (k) k->abort();
+    return rc;
 }
 
 void comm_release(gbs_ctx* c) {

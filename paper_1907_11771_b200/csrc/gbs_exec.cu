@@ -518,8 +518,17 @@ static int enqueue_macro(gbs_ctx* c, double H) {
 
 extern "C" {
 
+static int advance_impl(gbs_ctx* c, int64_t macro_steps, double H);
+
+// a rank of the local transport that fails wakes the members waiting for it in a collective
 int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
     if (!c) return fail(c, GBS_E_INVAL, "ctx is NULL");
+    return comm_abort_on_error(c, advance_impl(c, macro_steps, H));
+}
+
+}  // extern "C"
+
+static int advance_impl(gbs_ctx* c, int64_t macro_steps, double H) {
     if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_advance before gbs_write_state");
     if (macro_steps < 0) return fail(c, GBS_E_INVAL, "macro_steps=%lld < 0", (long long)macro_steps);
     if (!(H > 0.0) || !std::isfinite(H)) return fail(c, GBS_E_INVAL, "H=%g must be positive and finite", H);
@@ -575,5 +584,3 @@ int gbs_advance(gbs_ctx* c, int64_t macro_steps, double H) {
     }
     return GBS_OK;
 }
-
-}  // extern "C"

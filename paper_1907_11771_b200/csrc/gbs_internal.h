@@ -94,10 +94,14 @@ struct Comm {
     // member i's context when the members share this process (local transport), else nullptr
     virtual gbs_ctx* member_ctx(int) { return nullptr; }
     virtual void register_ctx(gbs_ctx*) {}
+    // local transport: wake every member blocked in a collective of this communicator with an
+    // error (a rank that failed will not arrive); NCCL: nothing (ncclCommAbort is the caller's)
+    virtual void abort() {}
 };
 int comm_init(gbs_ctx* c, const gbs_dist* d);   // world, slab and group communicators
 int comm_nccl_self(gbs_ctx* c, Comm** out);      // one-rank NCCL communicator (loopback_nccl)
 void comm_release(gbs_ctx* c);
+int comm_abort_on_error(gbs_ctx* c, int rc);     // rc != GBS_OK: abort the local communicators
 
 // ---------------------------------------------------------------------------
 struct Slab {

@@ -114,7 +114,15 @@ int gbs_sync(gbs_ctx* c) {
     return check_flag(c);
 }
 
+static int read_state_impl(gbs_ctx* c, double* dst, int64_t count, int on_device);
+
 int gbs_read_state(gbs_ctx* c, double* dst, int64_t count, int on_device) {
+    return comm_abort_on_error(c, read_state_impl(c, dst, count, on_device));
+}
+
+}  // extern "C"
+
+static int read_state_impl(gbs_ctx* c, double* dst, int64_t count, int on_device) {
     if (!c || !dst) return fail(c, GBS_E_INVAL, "ctx or dst is NULL");
     if (!c->have_state) return fail(c, GBS_E_STATE, "gbs_read_state before gbs_write_state");
     if (count != c->F * c->points)
@@ -143,6 +151,8 @@ int gbs_read_state(gbs_ctx* c, double* dst, int64_t count, int on_device) {
     if (rc) return rc;
     return harvest_timer(c);
 }
+
+extern "C" {
 
 int gbs_write_slab(gbs_ctx* c, const double* src, int64_t count, int on_device) {
     if (!c || !src) return fail(c, GBS_E_INVAL, "ctx or src is NULL");

@@ -287,3 +287,33 @@ def test_c5_full_size_eight_ranks_match_one_context(torch_cuda, groups, fused):
         else:
             rel, _, mmax = errors(out, part)
             assert rel <= TOL and mmax <= TOL_ELEM
+
+
+def test_failed_rank_releases_the_others(torch_cuda):
+    """A rank whose gbs_advance fails (here: an invalid H) marks its local communicators broken,
+    so the other ranks blocked in a collective fail at once instead of after the 300 s timeout."""
+    import time
+    from paper_1907_11771_b200 import gbs
+    w = reduced("c4", (64, 32, 48), macro_steps=1, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8", "c4")
+    y0 = make_ic(w)
+    codes = [None, None]
+
+    def body(dist):
+        torch_cuda.cuda.set_device(0)
+        s = torch_cuda.cuda.Stream()
+        with gbs.Stepper(w.pde, w.n, w.order, counts, wd, dist=dist, stream=s.cuda_stream) as st:
+            st.write(y0)
+            try:
+                st.advance(2, H if dist["rank"] == 0 else -1.0)
+                st.sync()
+                out = np.empty_like(y0)
+                st.read(out)
+            except gbs.GbsError as e:
+                codes[dist["rank"]] = e.code
+        return True
+
+    t0 = time.time()
+    gbs.run_local_ranks(2, body, groups=1)
+    assert time.time() - t0 < 120
+    assert codes[1] == gbs.GBS_E_INVAL and codes[0] == gbs.GBS_E_NCCL
