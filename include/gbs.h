@@ -104,7 +104,8 @@ typedef struct gbs_dist {
 /* In-process transport for `world` contexts on one device (GBS_TRANSPORT_LOCAL): create the
  * hub once, pass it in every rank's gbs_dist, call gbs_create / gbs_advance / gbs_read_state
  * of the ranks from `world` concurrent host threads (collectives block until every member of
- * the communicator arrives; a member missing for 300 s fails them with GBS_E_NCCL), destroy
+ * the communicator arrives; a member whose gbs_advance / gbs_read_state fails releases them at
+ * once, and one missing for 300 s fails them, both with GBS_E_NCCL), destroy
  * the hub after every context.  The macro step runs the same plan, halo schedule, group
  * combine and gather as over NCCL: halo planes by device-to-device copies matched in NCCL's
  * posting order, the combine as one kernel per rank that sums its share of the elements over
