@@ -313,6 +313,11 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        as lap(u_0) + h lap(v_0) -- a rounding-level change; default 1)
  *   "half_tall"    1/0   64 x 32 tiles for the half kernel when ny % 32 == 0 (default 1)
  *   "half_rpt"     2/4   rows per thread of the tall half kernel (16 or 8 warps; default 4)
+ *   "zchunk_fin"   k     planes per CTA of the LF + final pass only (0 = as the pair; default 0)
+ *   "l2hint_fin"   bits  the LF + final pass's L2 policy bits (as "l2hint"; default 11)
+ *   "streams"      1/2   sequences alternating over two CUDA streams on single-substep paths with
+ *                        spare level buffers (2-D TMA grids, 3-D with fuse 0); final passes kept in
+ *                        ascending n_k order by events, bit-identical (default 1: measured no faster)
  *   "l2hint_half"  bits  half kernel: 1 centre boxes evict_last, 2 streaming loads of the
  *                        pointwise field, 4 halo boxes evict_first, 8 streaming stores (default 11)
  *   "fuse2d"       1/0   2-D acoustics: two substeps per pass as the chain-U / chain-P
@@ -348,7 +353,8 @@ GBS_API int gbs_set_option(gbs_ctx* ctx, const char* key, int64_t value);
  * since the last reset: cls 0 = interior LF, 1 = FE, 2 = final (average + weighted
  * accumulate), 3 = two LF substeps in one pass, 4 = LF + final in one pass, 5 = the
  * whole-run cluster kernel, 6 = one single-stencil-field half of a two-substep pass
- * (option "half").  reset = 1 clears the counters after reading. */
+ * (option "half"), 7 = the forward Euler fused with the first chain step (option "fea").
+ * reset = 1 clears the counters after reading. */
 GBS_API int gbs_kernel_time(gbs_ctx* ctx, int cls, double* total_ms, int64_t* launches, int reset);
 
 GBS_API const char* gbs_strerror(int code);
