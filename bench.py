@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -308,7 +309,8 @@ def run_ours(a):
         # all macro steps of a gbs_advance in one launch), where one step is the config's whole
         # run (w.macro_steps macro steps, one launch).
         whole_run = w.ndim == 1 and a.warmup >= 1 and st.info()["kernel_launches"] == 1
-        run_len = w.macro_steps if whole_run else 1
+        # (s41: macro_steps 0 = "once around the period", ceil(1 / H) macro steps, DESIGN R22)
+        run_len = (w.macro_steps if w.macro_steps > 0 else math.ceil(1.0 / H)) if whole_run else 1
         # Working sets that fit in L2 (C1, C2) are timed step by step with an L2 flush (a
         # 512 MiB write) before every timed step; larger ones run back to back.
         L2_BYTES = 126 * 2 ** 20
