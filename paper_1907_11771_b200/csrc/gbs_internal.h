@@ -198,6 +198,7 @@ struct gbs_ctx {
     int zchunk_fin_opt = 0;           // the same for its LF + final pass only (0 = as above)
     int hint_fin_opt = 11;            // L2 policy bits of the LF + final pass (PairArgs::hint)
     int n_streams = 1;                // sequence streams (option "streams": 1 or 2)
+    bool fea_ring = false;            // that pass with both fields fed through tile rings
     bool use_fea = true;              // FE fused with chain A's first step (option "fea"; C5:
                                       // 12.3 ms instead of 7.55 + 5.96, macro step 506 -> 492 ms)
     cudaStream_t stream2 = nullptr;

@@ -295,3 +295,237 @@ wave3d_half_tma(const __grid_constant__ HalfMaps M, const HalfArgs A, const int 
 
 }  // namespace tma
 }  // namespace gbs
+
+namespace gbs {
+namespace tma {
+
+// ---------------------------------------------------------------------------
+// The forward Euler fused with the first step of chain A (gbs_wave3d_pair.cuh MODE_FEA, the
+// same operations in the same order, so bit-identical to it) with both stencil fields u_0, v_0
+// fed through rings of R + D tiles: the queue fronts (plane z + R) are read from the ring
+// instead of being loaded again as separate centre boxes -- 26.6 KB of TMA writes per plane
+// instead of 42.6, no L2 re-reads of the fronts.  64 x 16 tiles, 8 warps x 2 x 2 points, two
+// register queues (as the pair kernel), D = 4 stages in 213 KB.
+// ---------------------------------------------------------------------------
+struct FeaMaps {
+    HalfMaps u, v;                    // u_0, v_0: centre TX x TY, y halos TX x R, x strips R x TY
+};
+
+struct FeaArgs {
+    const double* U0; const double* V0;
+    double* V1; double* U2; double* V2; double* U3;
+    int nx, ny, nz, zchunk;
+    int zlo, zhi, zskip;
+    int64_t plane;
+    double sx2, sy2, sz2;
+    double h, h2;                     // h, 2h
+    int band;
+    int hint;                         // 1 centre boxes evict_last, 4 halo boxes evict_first, 8 .cs stores
+};
+
+template <int R, bool SLAB, int D>
+__global__ void __launch_bounds__(256, 1)
+wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zbase) {
+    using L = HalfLayout<R, TY, D>;
+    constexpr int NW = TY / 2;                 // 8 warps, 2 rows x 2 columns per thread
+    constexpr int RING = L::RING, TILE = L::TILE;
+    constexpr int Q = 2 * R + 1;
+    extern __shared__ __align__(128) double smem[];
+    double* ringu = smem;
+    double* ringv = smem + L::ring_doubles;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * L::ring_doubles);
+    uint64_t* empty = full + D;
+    uint64_t* init = empty + D;
+
+    const int tx = threadIdx.x, ty = threadIdx.y, lane = tx;
+    const int nx = A.nx, ny = A.ny, nz = A.nz;
+    int xt, yt;
+    tile_of(blockIdx.x, nx / TX, ny / TY, A.band, xt, yt);
+    const int x0 = xt * TX, y0 = yt * TY;
+    const int z0 = A.zlo + blockIdx.z * A.zchunk + (blockIdx.z ? A.zskip : 0);
+    const int niter = min(A.zchunk, A.zhi - z0);
+    auto zc = [&](int z) -> int {
+        if constexpr (SLAB) return z + zbase;
+        else return wrap_once(z, nz);
+    };
+    const bool producer = (ty == 0 && lane == 0);
+    const int ytop = wrap_any(y0 - R, ny), ybot = wrap_any(y0 + TY, ny);
+    const int xl = wrap_any(x0 - R, nx), xr = wrap_any(x0 + TX, nx);
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    auto ld = [&](void* dst, const CUtensorMap* m, int x, int y, int z, uint64_t* bar, int bit, uint64_t pol) {
+        if (A.hint & bit) tma_load_3d_hint(dst, m, x, y, z, bar, pol);
+        else tma_load_3d(dst, m, x, y, z, bar);
+    };
+    auto issue_tile = [&](double* ring, const HalfMaps& m, int p, uint64_t* bar) {
+        double* t = ring + (size_t)(p % RING) * TILE;
+        const int z = zc(z0 + p);
+        ld(t, &m.x_b, x0, ytop, z, bar, 4, pol_first);
+        ld(t + R * TX, &m.x_a, x0, y0, z, bar, 1, pol_last);
+        ld(t + (R + TY) * TX, &m.x_b, x0, ybot, z, bar, 4, pol_first);
+        ld(t + L::CENTER, &m.x_c, xl, y0, z, bar, 4, pol_first);
+        ld(t + L::CENTER + L::STRIP, &m.x_c, xr, y0, z, bar, 4, pol_first);
+    };
+    auto issue_stage = [&](int k) {              // the tiles of plane k + R, both fields
+        const int s = k % D;
+        if (k >= D) mbar_wait(&empty[s], (uint32_t)(((k / D) - 1) & 1));
+        mbar_expect_tx(&full[s], 2 * L::tile_bytes);
+        issue_tile(ringu, M.u, k + R, &full[s]);
+        issue_tile(ringv, M.v, k + R, &full[s]);
+    };
+    if (producer) {
+        for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
+        mbar_init(init, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (producer) {
+        prefetch_map(&M.u.x_a); prefetch_map(&M.u.x_b); prefetch_map(&M.u.x_c);
+        prefetch_map(&M.v.x_a); prefetch_map(&M.v.x_b); prefetch_map(&M.v.x_c);
+        mbar_expect_tx(init, 2 * R * L::tile_bytes);
+        for (int p = 0; p < R; ++p) { issue_tile(ringu, M.u, p, init); issue_tile(ringv, M.v, p, init); }
+        for (int k = 0; k < D - 1 && k < niter; ++k) issue_stage(k);
+    }
+
+    const int64_t plane = A.plane;
+    const int r0 = 2 * ty;
+    const int64_t own = (int64_t)(y0 + r0) * nx + x0 + 2 * tx;
+    auto zoff = [&](int z) -> int64_t {
+        if constexpr (SLAB) return (int64_t)z * plane;
+        else return (int64_t)wrap_once(z, nz) * plane;
+    };
+    // queues of u_0 and v_0 at planes z - R .. z + R; point index 2*row + col
+    double qs[Q][4], qa[Q][4];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int64_t oz = zoff(z0 - R + j);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int64_t o = oz + own + (int64_t)r * nx;
+            const double2 su = __ldg(reinterpret_cast<const double2*>(A.U0 + o));
+            const double2 uu = __ldg(reinterpret_cast<const double2*>(A.V0 + o));
+            qs[j][2 * r] = su.x; qs[j][2 * r + 1] = su.y;
+            qa[j][2 * r] = uu.x; qa[j][2 * r + 1] = uu.y;
+        }
+    }
+    const int crow0 = (R + r0) * TX + 2 * tx;
+    mbar_wait(init, 0);
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const double2 a = *reinterpret_cast<const double2*>(ringu + (size_t)j * TILE + crow0 + r * TX);
+            const double2 b = *reinterpret_cast<const double2*>(ringv + (size_t)j * TILE + crow0 + r * TX);
+            qs[R + j][2 * r] = a.x; qs[R + j][2 * r + 1] = a.y;
+            qa[R + j][2 * r] = b.x; qa[R + j][2 * r + 1] = b.y;
+        }
+    int woff[2][R + 1];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int k = 0; k <= R; ++k) {
+            const int col = 2 * tx - R + 2 * k, row = r0 + r;
+            woff[r][k] = col < 0 ? L::CENTER + row * R + (col + R)
+                       : col >= TX ? L::CENTER + L::STRIP + row * R + (col - TX)
+                                   : (R + row) * TX + col;
+        }
+    // lap at the 4 points: the pair kernel's lap4, same sums in the same order
+    auto lap4 = [&](const double* tile, const double (*q)[4], double* lap, double* cen) {
+        double lx[4], ly[4], lz[4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            double xw[2 * R + 2];
+#pragma unroll
+            for (int k = 0; k <= R; ++k) {
+                if (k == R / 2) {
+                    xw[2 * k] = q[R][2 * r]; xw[2 * k + 1] = q[R][2 * r + 1];
+                    continue;
+                }
+                const double2 a = *reinterpret_cast<const double2*>(tile + woff[r][k]);
+                xw[2 * k] = a.x; xw[2 * k + 1] = a.y;
+            }
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int p = 2 * r + v;
+                cen[p] = xw[R + v];
+                lx[p] = FD<R>::b0() * xw[R + v];
+#pragma unroll
+                for (int j = 1; j <= R; ++j) lx[p] = fma(FD<R>::b(j), xw[R + v + j] + xw[R + v - j], lx[p]);
+                ly[p] = FD<R>::b0() * xw[R + v];
+                lz[p] = ly[p];
+            }
+        }
+        double prev_up[2], prev_dn[2];
+#pragma unroll
+        for (int j = 1; j <= R; ++j) {
+            const double2 u = *reinterpret_cast<const double2*>(tile + crow0 - j * TX);
+            const double2 d = *reinterpret_cast<const double2*>(tile + crow0 + (1 + j) * TX);
+            const double up0[2] = {u.x, u.y}, dn1[2] = {d.x, d.y};
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const double dn0 = (j == 1) ? cen[2 + v] : prev_dn[v];
+                const double up1 = (j == 1) ? cen[v] : prev_up[v];
+                ly[v] = fma(FD<R>::b(j), dn0 + up0[v], ly[v]);
+                ly[2 + v] = fma(FD<R>::b(j), dn1[v] + up1, ly[2 + v]);
+                prev_up[v] = up0[v];
+                prev_dn[v] = dn1[v];
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+#pragma unroll
+            for (int j = 1; j <= R; ++j) lz[p] = fma(FD<R>::b(j), q[R + j][p] + q[R - j][p], lz[p]);
+            lap[p] = fma(A.sx2, lx[p], fma(A.sy2, ly[p], A.sz2 * lz[p]));
+        }
+    };
+
+    const bool scs = A.hint & 8;
+    auto put = [&](double* p, double a, double b) {
+        if (scs) __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
+        else *reinterpret_cast<double2*>(p) = make_double2(a, b);
+    };
+    for (int i = 0; i < niter; ++i) {
+        const int s = i % D;
+        if (producer && i + D - 1 < niter) issue_stage(i + D - 1);
+        mbar_wait(&full[s], (uint32_t)((i / D) & 1));
+        const size_t cur = (size_t)(i % RING) * TILE, fr = (size_t)((i + R) % RING) * TILE;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const double2 a = *reinterpret_cast<const double2*>(ringu + fr + crow0 + r * TX);
+            const double2 b = *reinterpret_cast<const double2*>(ringv + fr + crow0 + r * TX);
+            qs[2 * R][2 * r] = a.x; qs[2 * R][2 * r + 1] = a.y;
+            qa[2 * R][2 * r] = b.x; qa[2 * R][2 * r + 1] = b.y;
+        }
+        double lapS[4], lapU[4], xs_c[4], xu_c[4];
+        lap4(ringu + cur, qs, lapS, xs_c);
+        lap4(ringv + cur, qa, lapU, xu_c);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        double va[4], ub[4], vb[4], uc[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {                // as wave3d_pair_tma MODE_FEA
+            const double u0 = xs_c[p], v0 = xu_c[p];
+            vb[p] = combine<MODE_FE>(0.0, v0, lapS[p], 0.0, A.h, 0.0);        // v_1
+            const double u1 = combine<MODE_FE>(0.0, u0, v0, 0.0, A.h, 0.0);   // u_1
+            uc[p] = combine<MODE_LF>(u0, 0.0, vb[p], 0.0, A.h2, 0.0);         // u_2
+            const double lap1 = fma(A.h, lapU[p], lapS[p]);                    // lap(u_1)
+            va[p] = combine<MODE_LF>(v0, 0.0, lap1, 0.0, A.h2, 0.0);           // v_2
+            ub[p] = combine<MODE_LF>(u1, 0.0, va[p], 0.0, A.h2, 0.0);          // u_3
+        }
+        const int64_t oz = zoff(z0 + i);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int64_t o = oz + own + (int64_t)r * nx;
+            put(A.V2 + o, va[2 * r], va[2 * r + 1]);
+            put(A.U3 + o, ub[2 * r], ub[2 * r + 1]);
+            put(A.V1 + o, vb[2 * r], vb[2 * r + 1]);
+            put(A.U2 + o, uc[2 * r], uc[2 * r + 1]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * R; ++j)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) { qs[j][p] = qs[j + 1][p]; qa[j][p] = qa[j + 1][p]; }
+    }
+}
+
+}  // namespace tma
+}  // namespace gbs

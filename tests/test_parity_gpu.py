@@ -234,6 +234,16 @@ def test_half_kernels_bitwise_equal_coupled_pair(torch_cuda, cfg, n, opts):
                                         ("c5", (64, 64, 48), {"loopback": 3}), ("c4", (64, 16, 9), {}),
                                         ("c4", (64, 32, 24), {"loopback": 2, "overlap": 0, "graph": 0})])
 def test_fe_fused_with_first_chain_step(torch_cuda, cfg, n, opts):
+    _fea_case(torch_cuda, cfg, n, opts)
+    # the ring-fed variant of the same pass: the same operations, bit-identical
+    w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
+    counts, wd, H = scheme_for(w, "nonzero8")
+    _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1, fea_ring=1))
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1, fea_ring=0))
+    assert np.array_equal(a[0], b[0])
+
+
+def _fea_case(torch_cuda, cfg, n, opts):
     """Option fea: the FE fused with the first step of one leap-frog chain (lap(u_1) by
     linearity, gbs_wave3d_pair.cuh MODE_FEA) -- a rounding-level change, so against the oracle
     and the unfused path within the parity bar, and one launch fewer per sequence with n >= 4."""
