@@ -179,6 +179,7 @@ int gbs_set_option(gbs_ctx* c, const char* key, int64_t value) {
     if (k == "l2hint") { c->hint_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "l2hint_step") { c->hint_step_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
     if (k == "band") { c->band_opt = (int)std::max<int64_t>(0, value); drop_graphs(); return GBS_OK; }
+    if (k == "fin_ring") { c->fin_ring = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fea_ring") { c->fea_ring = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "fea") { c->use_fea = value != 0; drop_graphs(); return GBS_OK; }
     if (k == "streams") {

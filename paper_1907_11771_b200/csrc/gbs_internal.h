@@ -199,6 +199,7 @@ struct gbs_ctx {
     int hint_fin_opt = 11;            // L2 policy bits of the LF + final pass (PairArgs::hint)
     int n_streams = 1;                // sequence streams (option "streams": 1 or 2)
     bool fea_ring = false;            // that pass with both fields fed through tile rings
+    bool fin_ring = false;            // the LF + final pass fed through tile rings (2 stages)
     bool use_fea = true;              // FE fused with chain A's first step (option "fea"; C5:
                                       // 12.3 ms instead of 7.55 + 5.96, macro step 506 -> 492 ms)
     cudaStream_t stream2 = nullptr;

@@ -475,51 +475,71 @@ int launch_step(gbs_ctx* c, Slab& s, const StepOperands& op, int64_t lo, int64_t
     return GBS_OK;
 }
 
-// the fused FE + first chain step with both fields fed through tile rings (wave3d_fea_ring)
-template <int R, bool SLAB>
-static cudaError_t launch_fea_ring_k(const gbs::tma::FeaMaps& m, const gbs::tma::FeaArgs& a, int zbase, dim3 grid,
-                                     cudaStream_t st) {
-    constexpr int D = 4;
-    using L = gbs::tma::HalfLayout<R, gbs::tma::TY, D>;
-    constexpr size_t bytes = 2 * L::ring_doubles * 8 + (2 * D + 1) * 8;
-    auto k = gbs::tma::wave3d_fea_ring<R, SLAB, D>;
-    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), bytes);
+// the two-laplacian passes with both stencil fields fed through tile rings (wave3d_ring2):
+// the fused FE + first chain step, and the LF + final pass
+template <int R, int MODE, bool SLAB>
+static cudaError_t launch_ring2_k(const gbs::tma::Ring2Maps& m, const gbs::tma::Ring2Args& a, int zbase, dim3 grid,
+                                  cudaStream_t st) {
+    using RL = gbs::tma::Ring2Layout<R, MODE>;
+    auto k = gbs::tma::wave3d_ring2<R, MODE, SLAB>;
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), RL::bytes);
     if (e != cudaSuccess) return e;
-    k<<<grid, dim3(32, gbs::tma::TY / 2), bytes, st>>>(m, a, zbase);
+    k<<<grid, dim3(32, gbs::tma::TY / 2), RL::bytes, st>>>(m, a, zbase);
     return cudaSuccess;
 }
 
-static int launch_fea_ring(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi, int64_t gap) {
+static int launch_ring2(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi, int64_t gap) {
     const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;
-    gbs::tma::FeaArgs a{};
-    a.U0 = field_ptr(c, s, op.Su.b, op.Su.f);
-    a.V0 = field_ptr(c, s, op.U.b, op.U.f);
-    a.V2 = field_ptr(c, s, op.Av.b, op.Av.f);
-    a.U3 = field_ptr(c, s, op.Bu.b, op.Bu.f);
-    a.V1 = field_ptr(c, s, op.Bv.b, op.Bv.f);
-    a.U2 = field_ptr(c, s, op.Cu.b, op.Cu.f);
+    const bool fea = op.modeB == gbs::tma::MODE_FEA;
+    gbs::tma::Ring2Args a{};
+    a.Su = field_ptr(c, s, op.Su.b, op.Su.f);
+    a.U = field_ptr(c, s, op.U.b, op.U.f);
+    if (fea) {
+        a.A2 = field_ptr(c, s, op.Av.b, op.Av.f);
+        a.A3 = field_ptr(c, s, op.Bu.b, op.Bu.f);
+        a.A1 = field_ptr(c, s, op.Bv.b, op.Bv.f);
+        a.A4 = field_ptr(c, s, op.Cu.b, op.Cu.f);
+    } else {
+        a.A3 = op.out_u ? op.out_u : field_ptr(c, s, op.Bu.b, 0);
+        a.A1 = op.out_v ? op.out_v : field_ptr(c, s, op.Bu.b, 1);
+    }
     a.nx = (int)c->n[0]; a.ny = (int)c->n[1]; a.nz = (int)s.nz;
     a.plane = c->plane;
     const double sx = c->n[0] / c->len[0], sy = c->n[1] / c->len[1], sz = c->n[2] / c->len[2];
     a.sx2 = sx * sx; a.sy2 = sy * sy; a.sz2 = sz * sz;
-    a.h = op.cfA; a.h2 = op.cfB;
+    a.cfA = op.cfA; a.cfB = op.cfB; a.wh = op.wh;
+    a.nonfinite = op.flag ? c->d_flag : nullptr;
     a.zlo = (int)lo; a.zhi = (int)hi;
     const int64_t tiles = (c->n[0] / gbs::tma::TX) * (c->n[1] / gbs::tma::TY);
     const int zauto = tiles * ((hi - lo + 255) / 256) >= 8LL * c->sms ? 256 : 128;
-    const int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : zauto;
+    int zc = c->zchunk_pair_opt > 0 ? c->zchunk_pair_opt : c->zchunk_opt > 0 ? c->zchunk_opt : zauto;
+    if (!fea && c->zchunk_fin_opt > 0) zc = c->zchunk_fin_opt;
     a.zchunk = (int)std::min<int64_t>(zc, hi - lo);
     a.band = tile_band(c, c->n[0] / gbs::tma::TX);
-    a.hint = c->hint_opt;
+    a.hint = fea ? c->hint_opt : c->hint_fin_opt;
     dim3 grid((unsigned)tiles, 1u, (unsigned)((hi - lo + a.zchunk - 1) / a.zchunk));
     face_chunks(lo, hi, gap, a.zchunk, a.zskip, grid.z);
-    gbs::tma::FeaMaps m;
+    gbs::tma::Ring2Maps m;
     m.u.x_a = s.tm[op.Su.b][op.Su.f][0]; m.u.x_b = s.tm[op.Su.b][op.Su.f][1]; m.u.x_c = s.tm[op.Su.b][op.Su.f][2];
     m.v.x_a = s.tm[op.U.b][op.U.f][0]; m.v.x_b = s.tm[op.U.b][op.U.f][1]; m.v.x_c = s.tm[op.U.b][op.U.f][2];
+    if (!fea) {
+        m.sv = s.tm[op.Sv.b][op.Sv.f][0];
+        m.pv = s.tm[op.Pv.b][op.Pv.f][0];
+        m.acc_u = s.tm[op.Bu.b][0][0];
+        m.acc_v = s.tm[op.Bu.b][1][0];
+    }
     const int zbase = (int)c->ghost;
-    cudaError_t e;
-    if (c->R == 2) e = slab ? launch_fea_ring_k<2, true>(m, a, zbase, grid, c->stream) : launch_fea_ring_k<2, false>(m, a, zbase, grid, c->stream);
-    else e = slab ? launch_fea_ring_k<4, true>(m, a, zbase, grid, c->stream) : launch_fea_ring_k<4, false>(m, a, zbase, grid, c->stream);
-    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "fea ring kernel setup: %s", cudaGetErrorString(e));
+    cudaError_t e = cudaSuccess;
+#define RG(RR, SL)                                                                                  \
+    switch (op.modeB) {                                                                             \
+        case gbs::tma::MODE_FEA: e = launch_ring2_k<RR, gbs::tma::MODE_FEA, SL>(m, a, zbase, grid, c->stream); break; \
+        case gbs::MODE_FIN0: e = launch_ring2_k<RR, gbs::MODE_FIN0, SL>(m, a, zbase, grid, c->stream); break;         \
+        default: e = launch_ring2_k<RR, gbs::MODE_FINACC, SL>(m, a, zbase, grid, c->stream); break;                    \
+    }
+    if (c->R == 2) { if (slab) { RG(2, true) } else { RG(2, false) } }
+    else { if (slab) { RG(4, true) } else { RG(4, false) } }
+#undef RG
+    if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "ring2 kernel setup: %s", cudaGetErrorString(e));
     c->launches++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(c, GBS_E_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
@@ -527,7 +547,9 @@ static int launch_fea_ring(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t 
 }
 
 int launch_pair(gbs_ctx* c, Slab& s, const PairOperands& op, int64_t lo, int64_t hi, int64_t gap) {
-    if (op.modeB == gbs::tma::MODE_FEA && c->fea_ring && !c->peer_on) return launch_fea_ring(c, s, op, lo, hi, gap);
+    if (!c->peer_on && ((op.modeB == gbs::tma::MODE_FEA && c->fea_ring) ||
+                        ((op.modeB == gbs::MODE_FIN0 || op.modeB == gbs::MODE_FINACC) && c->fin_ring)))
+        return launch_ring2(c, s, op, lo, hi, gap);
     // slab kernels read ghost planes refreshed from neighbours; one slab (2-D TMA grids keep
     // ghost rows for the two-substep kernels) wraps periodically like a plain grid
     const bool slab = c->ghost > 0 && c->slabs * c->loopback > 1;

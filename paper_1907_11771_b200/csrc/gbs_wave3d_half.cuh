@@ -37,6 +37,7 @@
 #pragma once
 
 #include "gbs_wave3d_tma.cuh"
+#include "gbs_wave3d_pair.cuh"      // MODE_FEA
 
 namespace gbs {
 namespace tma {
@@ -300,40 +301,62 @@ namespace gbs {
 namespace tma {
 
 // ---------------------------------------------------------------------------
-// The forward Euler fused with the first step of chain A (gbs_wave3d_pair.cuh MODE_FEA, the
-// same operations in the same order, so bit-identical to it) with both stencil fields u_0, v_0
-// fed through rings of R + D tiles: the queue fronts (plane z + R) are read from the ring
-// instead of being loaded again as separate centre boxes -- 26.6 KB of TMA writes per plane
-// instead of 42.6, no L2 re-reads of the fronts.  64 x 16 tiles, 8 warps x 2 x 2 points, two
-// register queues (as the pair kernel), D = 4 stages in 213 KB.
+// The two-laplacian passes of the 3-D path with both stencil fields fed through rings of
+// R + D tiles (the queue fronts, plane z + R, are read from the ring instead of being loaded
+// again as separate centre boxes).  The same operations in the same order as
+// gbs_wave3d_pair.cuh, so bit-identical to it:
+//   MODE_FEA     the forward Euler fused with the first step of chain A: fields u_0, v_0;
+//                outputs A2 = v_2, A3 = u_3, A1 = v_1, A4 = u_2 (D = 4, 213 KB)
+//   MODE_FIN0/   the last leap-frog step + averaging + weighted accumulate: fields S_u, U and
+//   MODE_FINACC  the pointwise boxes S_v, P_v (+ the accumulator) of plane z; outputs the
+//                accumulator's u, v (A3, A1 pointers) (D = 2, 224 KB)
+// 64 x 16 tiles, 8 warps x 2 x 2 points, two register queues (as the pair kernel).
 // ---------------------------------------------------------------------------
-struct FeaMaps {
-    HalfMaps u, v;                    // u_0, v_0: centre TX x TY, y halos TX x R, x strips R x TY
+struct Ring2Maps {
+    HalfMaps u, v;                    // the two stencil fields: centre TX x TY, y halos, x strips
+    CUtensorMap sv, pv, acc_u, acc_v; // FIN: TX x TY boxes
 };
 
-struct FeaArgs {
-    const double* U0; const double* V0;
-    double* V1; double* U2; double* V2; double* U3;
+struct Ring2Args {
+    const double* Su; const double* U;   // the two stencil fields (queue seeds)
+    double* A1; double* A2; double* A3; double* A4;
     int nx, ny, nz, zchunk;
     int zlo, zhi, zskip;
     int64_t plane;
     double sx2, sy2, sz2;
-    double h, h2;                     // h, 2h
+    double cfA, cfB, wh;
+    int* nonfinite;
     int band;
-    int hint;                         // 1 centre boxes evict_last, 4 halo boxes evict_first, 8 .cs stores
+    int hint;                         // 1 centre boxes evict_last, 2 pointwise boxes evict_first,
+                                      // 4 halo boxes evict_first, 8 .cs stores
 };
 
-template <int R, bool SLAB, int D>
+template <int R, int MODE>
+struct Ring2Layout {
+    static constexpr bool FIN = MODE != MODE_FEA;
+    static constexpr int NPW = FIN ? (MODE == MODE_FINACC ? 4 : 2) : 0;
+    static constexpr int D = FIN ? 2 : 4;
+    using T = HalfLayout<R, TY, D>;
+    static constexpr int PWT = TY * TX;
+    static constexpr size_t pw_doubles = (size_t)D * NPW * PWT;
+    static constexpr size_t bytes = (2 * T::ring_doubles + pw_doubles) * 8 + (2 * D + 1) * 8;
+    static constexpr uint32_t stage_bytes = 2 * T::tile_bytes + NPW * PWT * 8;
+};
+
+template <int R, int MODE, bool SLAB>
 __global__ void __launch_bounds__(256, 1)
-wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zbase) {
-    using L = HalfLayout<R, TY, D>;
+wave3d_ring2(const __grid_constant__ Ring2Maps M, const Ring2Args A, const int zbase) {
+    using RL = Ring2Layout<R, MODE>;
+    using L = typename RL::T;
+    constexpr int D = RL::D, NPW = RL::NPW, PWT = RL::PWT;
     constexpr int NW = TY / 2;                 // 8 warps, 2 rows x 2 columns per thread
     constexpr int RING = L::RING, TILE = L::TILE;
     constexpr int Q = 2 * R + 1;
     extern __shared__ __align__(128) double smem[];
     double* ringu = smem;
     double* ringv = smem + L::ring_doubles;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * L::ring_doubles);
+    double* pw = smem + 2 * L::ring_doubles;   // [stage][S_v, P_v, acc_u, acc_v]
+    uint64_t* full = reinterpret_cast<uint64_t*>(pw + RL::pw_doubles);
     uint64_t* empty = full + D;
     uint64_t* init = empty + D;
 
@@ -365,12 +388,23 @@ wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zb
         ld(t + L::CENTER, &m.x_c, xl, y0, z, bar, 4, pol_first);
         ld(t + L::CENTER + L::STRIP, &m.x_c, xr, y0, z, bar, 4, pol_first);
     };
-    auto issue_stage = [&](int k) {              // the tiles of plane k + R, both fields
+    // stage k: the tiles of plane k + R (both rings) and the pointwise boxes of plane k
+    auto issue_stage = [&](int k) {
         const int s = k % D;
         if (k >= D) mbar_wait(&empty[s], (uint32_t)(((k / D) - 1) & 1));
-        mbar_expect_tx(&full[s], 2 * L::tile_bytes);
+        mbar_expect_tx(&full[s], RL::stage_bytes);
         issue_tile(ringu, M.u, k + R, &full[s]);
         issue_tile(ringv, M.v, k + R, &full[s]);
+        if constexpr (RL::FIN) {
+            double* p = pw + (size_t)s * NPW * PWT;
+            const int z = zc(z0 + k);
+            ld(p, &M.sv, x0, y0, z, &full[s], 2, pol_first);
+            ld(p + PWT, &M.pv, x0, y0, z, &full[s], 2, pol_first);
+            if constexpr (MODE == MODE_FINACC) {
+                ld(p + 2 * PWT, &M.acc_u, x0, y0, z, &full[s], 2, pol_first);
+                ld(p + 3 * PWT, &M.acc_v, x0, y0, z, &full[s], 2, pol_first);
+            }
+        }
     };
     if (producer) {
         for (int s = 0; s < D; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
@@ -381,6 +415,8 @@ wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zb
     if (producer) {
         prefetch_map(&M.u.x_a); prefetch_map(&M.u.x_b); prefetch_map(&M.u.x_c);
         prefetch_map(&M.v.x_a); prefetch_map(&M.v.x_b); prefetch_map(&M.v.x_c);
+        if constexpr (RL::FIN) { prefetch_map(&M.sv); prefetch_map(&M.pv); }
+        if constexpr (MODE == MODE_FINACC) { prefetch_map(&M.acc_u); prefetch_map(&M.acc_v); }
         mbar_expect_tx(init, 2 * R * L::tile_bytes);
         for (int p = 0; p < R; ++p) { issue_tile(ringu, M.u, p, init); issue_tile(ringv, M.v, p, init); }
         for (int k = 0; k < D - 1 && k < niter; ++k) issue_stage(k);
@@ -393,7 +429,7 @@ wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zb
         if constexpr (SLAB) return (int64_t)z * plane;
         else return (int64_t)wrap_once(z, nz) * plane;
     };
-    // queues of u_0 and v_0 at planes z - R .. z + R; point index 2*row + col
+    // queues of the two fields at planes z - R .. z + R; point index 2*row + col
     double qs[Q][4], qa[Q][4];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -401,8 +437,8 @@ wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zb
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int64_t o = oz + own + (int64_t)r * nx;
-            const double2 su = __ldg(reinterpret_cast<const double2*>(A.U0 + o));
-            const double2 uu = __ldg(reinterpret_cast<const double2*>(A.V0 + o));
+            const double2 su = __ldg(reinterpret_cast<const double2*>(A.Su + o));
+            const double2 uu = __ldg(reinterpret_cast<const double2*>(A.U + o));
             qs[j][2 * r] = su.x; qs[j][2 * r + 1] = su.y;
             qa[j][2 * r] = uu.x; qa[j][2 * r + 1] = uu.y;
         }
@@ -483,6 +519,7 @@ wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zb
         if (scs) __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
         else *reinterpret_cast<double2*>(p) = make_double2(a, b);
     };
+    bool bad = false;
     for (int i = 0; i < niter; ++i) {
         const int s = i % D;
         if (producer && i + D - 1 < niter) issue_stage(i + D - 1);
@@ -495,36 +532,71 @@ wave3d_fea_ring(const __grid_constant__ FeaMaps M, const FeaArgs A, const int zb
             qs[2 * R][2 * r] = a.x; qs[2 * R][2 * r + 1] = a.y;
             qa[2 * R][2 * r] = b.x; qa[2 * R][2 * r + 1] = b.y;
         }
+        double csv[4] = {0, 0, 0, 0}, cpv[4] = {0, 0, 0, 0}, cau[4] = {0, 0, 0, 0}, cav[4] = {0, 0, 0, 0};
+        if constexpr (RL::FIN) {
+            const double* p = pw + (size_t)s * NPW * PWT;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int po = (r0 + r) * TX + 2 * tx;
+                const double2 a = *reinterpret_cast<const double2*>(p + po);
+                const double2 b = *reinterpret_cast<const double2*>(p + PWT + po);
+                csv[2 * r] = a.x; csv[2 * r + 1] = a.y; cpv[2 * r] = b.x; cpv[2 * r + 1] = b.y;
+                if constexpr (MODE == MODE_FINACC) {
+                    const double2 c = *reinterpret_cast<const double2*>(p + 2 * PWT + po);
+                    const double2 d = *reinterpret_cast<const double2*>(p + 3 * PWT + po);
+                    cau[2 * r] = c.x; cau[2 * r + 1] = c.y; cav[2 * r] = d.x; cav[2 * r + 1] = d.y;
+                }
+            }
+        }
         double lapS[4], lapU[4], xs_c[4], xu_c[4];
         lap4(ringu + cur, qs, lapS, xs_c);
         lap4(ringv + cur, qa, lapU, xu_c);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        double va[4], ub[4], vb[4], uc[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {                // as wave3d_pair_tma MODE_FEA
-            const double u0 = xs_c[p], v0 = xu_c[p];
-            vb[p] = combine<MODE_FE>(0.0, v0, lapS[p], 0.0, A.h, 0.0);        // v_1
-            const double u1 = combine<MODE_FE>(0.0, u0, v0, 0.0, A.h, 0.0);   // u_1
-            uc[p] = combine<MODE_LF>(u0, 0.0, vb[p], 0.0, A.h2, 0.0);         // u_2
-            const double lap1 = fma(A.h, lapU[p], lapS[p]);                    // lap(u_1)
-            va[p] = combine<MODE_LF>(v0, 0.0, lap1, 0.0, A.h2, 0.0);           // v_2
-            ub[p] = combine<MODE_LF>(u1, 0.0, va[p], 0.0, A.h2, 0.0);          // u_3
-        }
         const int64_t oz = zoff(z0 + i);
+        if constexpr (MODE == MODE_FEA) {
+            double va[4], ub[4], vb[4], uc[4];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int64_t o = oz + own + (int64_t)r * nx;
-            put(A.V2 + o, va[2 * r], va[2 * r + 1]);
-            put(A.U3 + o, ub[2 * r], ub[2 * r + 1]);
-            put(A.V1 + o, vb[2 * r], vb[2 * r + 1]);
-            put(A.U2 + o, uc[2 * r], uc[2 * r + 1]);
+            for (int p = 0; p < 4; ++p) {            // as wave3d_pair_tma MODE_FEA
+                const double u0 = xs_c[p], v0 = xu_c[p];
+                vb[p] = combine<MODE_FE>(0.0, v0, lapS[p], 0.0, A.cfA, 0.0);        // v_1
+                const double u1 = combine<MODE_FE>(0.0, u0, v0, 0.0, A.cfA, 0.0);   // u_1
+                uc[p] = combine<MODE_LF>(u0, 0.0, vb[p], 0.0, A.cfB, 0.0);         // u_2
+                const double lap1 = fma(A.cfA, lapU[p], lapS[p]);                   // lap(u_1)
+                va[p] = combine<MODE_LF>(v0, 0.0, lap1, 0.0, A.cfB, 0.0);           // v_2
+                ub[p] = combine<MODE_LF>(u1, 0.0, va[p], 0.0, A.cfB, 0.0);          // u_3
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int64_t o = oz + own + (int64_t)r * nx;
+                put(A.A2 + o, va[2 * r], va[2 * r + 1]);
+                put(A.A3 + o, ub[2 * r], ub[2 * r + 1]);
+                put(A.A1 + o, vb[2 * r], vb[2 * r + 1]);
+                put(A.A4 + o, uc[2 * r], uc[2 * r + 1]);
+            }
+        } else {
+            double ub[4], vb[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {            // as wave3d_pair_tma FIN0 / FINACC
+                const double va = combine<MODE_LF>(cpv[p], csv[p], lapS[p], 0.0, A.cfA, 0.0);   // v_N
+                ub[p] = combine<MODE>(xs_c[p], xu_c[p], va, cau[p], A.cfB, A.wh);               // acc_u
+                vb[p] = combine<MODE>(csv[p], va, lapU[p], cav[p], A.cfB, A.wh);                // acc_v
+                bad |= !isfinite(ub[p]) || !isfinite(vb[p]);
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int64_t o = oz + own + (int64_t)r * nx;
+                put(A.A3 + o, ub[2 * r], ub[2 * r + 1]);
+                put(A.A1 + o, vb[2 * r], vb[2 * r + 1]);
+            }
         }
 #pragma unroll
         for (int j = 0; j < 2 * R; ++j)
 #pragma unroll
             for (int p = 0; p < 4; ++p) { qs[j][p] = qs[j + 1][p]; qa[j][p] = qa[j + 1][p]; }
     }
+    if constexpr (RL::FIN)
+        if (bad && A.nonfinite) *A.nonfinite = 1;
 }
 
 }  // namespace tma

@@ -238,8 +238,8 @@ def test_fe_fused_with_first_chain_step(torch_cuda, cfg, n, opts):
     # the ring-fed variant of the same pass: the same operations, bit-identical
     w = reduced(cfg, n, macro_steps=2, weights="nonzero8")
     counts, wd, H = scheme_for(w, "nonzero8")
-    _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1, fea_ring=1))
-    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1, fea_ring=0))
+    _, a, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1, fea_ring=1, fin_ring=1))
+    _, b, _ = run_gpu(torch_cuda, w, counts, wd, H, 2, opts=dict(opts, fea=1, fea_ring=0, fin_ring=0))
     assert np.array_equal(a[0], b[0])
 
 
