@@ -311,6 +311,9 @@ GBS_API int gbs_query(const gbs_ctx* ctx, gbs_info* info);
  *                        the first step of the u_1 leap-frog chain in one two-field pass (u_0, v_0 in;
  *                        v_1, u_2, v_2, u_3 out: 48 B per point instead of 40 + 32), lap(u_1) formed
  *                        as lap(u_0) + h lap(v_0) -- a rounding-level change; default 1)
+ *   "fea_ring"     1/0   that fused pass with both stencil fields fed through rings of tiles (the
+ *                        queue fronts read from the ring, not loaded again; bit-identical; default 1)
+ *   "fin_ring"     1/0   the same for the LF + final pass (2 stages fit; measured slower, default 0)
  *   "half_tall"    1/0   64 x 32 tiles for the half kernel when ny % 32 == 0 (default 1)
  *   "half_rpt"     2/4   rows per thread of the tall half kernel (16 or 8 warps; default 4)
  *   "zchunk_fin"   k     planes per CTA of the LF + final pass only (0 = as the pair; default 0)

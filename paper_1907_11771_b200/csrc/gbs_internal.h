@@ -198,8 +198,10 @@ struct gbs_ctx {
     int zchunk_fin_opt = 0;           // the same for its LF + final pass only (0 = as above)
     int hint_fin_opt = 11;            // L2 policy bits of the LF + final pass (PairArgs::hint)
     int n_streams = 1;                // sequence streams (option "streams": 1 or 2)
-    bool fea_ring = false;            // that pass with both fields fed through tile rings
-    bool fin_ring = false;            // the LF + final pass fed through tile rings (2 stages)
+    bool fea_ring = true;             // that pass with both fields fed through tile rings (C5: 10.8
+                                      // vs 11.0-11.3 ms per launch)
+    bool fin_ring = false;            // the LF + final pass fed through tile rings (only 2 stages
+                                      // fit: 13.1 vs 12.95 ms, off)
     bool use_fea = true;              // FE fused with chain A's first step (option "fea"; C5:
                                       // 12.3 ms instead of 7.55 + 5.96, macro step 506 -> 492 ms)
     cudaStream_t stream2 = nullptr;

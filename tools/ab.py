@@ -22,7 +22,7 @@ from paper_1907_11771_b200 import gbs, scheme  # noqa: E402
 CLS = ["lf", "fe", "fin", "lf2", "lffin", "cluster", "half", "fea"]
 # the library's defaults of the options a set may change (include/gbs.h)
 DEFAULTS = {"half": 1, "half_fe": 0, "half_tall": 1, "half_rpt": 4, "l2hint_half": 11, "l2hint": 11,
-            "l2hint_step": 0, "zchunk_fin": 0, "l2hint_fin": 11, "streams": 1, "fea": 1, "fea_ring": 0, "fin_ring": 0, "fuse": 1, "bulk": 1, "zchunk_pair": 0, "zchunk": 0, "band": 0, "overlap": 1}
+            "l2hint_step": 0, "zchunk_fin": 0, "l2hint_fin": 11, "streams": 1, "fea": 1, "fea_ring": 1, "fin_ring": 0, "fuse": 1, "bulk": 1, "zchunk_pair": 0, "zchunk": 0, "band": 0, "overlap": 1}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
